@@ -1,0 +1,130 @@
+/*
+ * trigpu.h -- C-ABI of the B200 (sm_100a) triangle-listing engine.
+ *
+ * Drop-in boundary for the reference trilist listing path. The reference's
+ * boundary is a C++ template API, not an ABI; each entry point below names the
+ * reference interface it replaces (paths under /root/reference/proj):
+ *
+ *   tl_orient / tl_orient_device
+ *       OrientedView::OrientedView(const Graph&, const Ordering&)
+ *       core/include/trilist/oriented_view.hpp:19, core/src/oriented_view.cpp:7-47
+ *   tl_list
+ *       list_app / list_apm (view, sink)          core/include/trilist/listing.hpp:162-173
+ *       list_app_parallel / list_apm_parallel     core/include/trilist/listing.hpp:187-199
+ *       ListingStats                              core/include/trilist/listing.hpp:23-34
+ *       (the GPU run is always "parallel": emission order is unspecified, as
+ *        listing.hpp:185-186 states for the parallel variants)
+ *   tl_fetch_triangles      CollectingSink::triangles   listing.hpp:46-56
+ *   tl_fetch_vertex_counts  new per-vertex sink
+ *   tl_fetch_oriented       OrientedView::successors / predecessors  oriented_view.hpp:24-29
+ *   tl_cost_report          cost_report(const OrientedView&)  core/src/cost.cpp:27-38
+ *
+ * Conventions: plain pointers and sizes, int status codes, no exceptions cross
+ * the ABI. Graph inputs are the reference Graph CSR (graph.hpp:59-60):
+ * offsets uint64[n+1], adjacency uint32[2m], each row strictly increasing by
+ * dense id; rank[v] = 0-based position of v (Ordering::ranks(),
+ * ordering.hpp:30). Everything that leaves the library is in dense ids.
+ * One context owns one CUDA stream and its device buffers; callers serialise
+ * use of a context; contexts are independent.
+ */
+#ifndef TRIGPU_H
+#define TRIGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define TL_API __attribute__((visibility("default")))
+#else
+#define TL_API
+#endif
+
+typedef struct tl_ctx tl_ctx;
+
+typedef enum {
+    TL_OK = 0,
+    TL_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference (oriented_view.cpp:8-9) */
+    TL_ERR_CUDA = 2,             /* no device, launch failure, ... */
+    TL_ERR_OUT_OF_MEMORY = 3,
+    TL_ERR_STATE = 4,            /* e.g. tl_list before tl_orient */
+    TL_ERR_CAPACITY = 5          /* caller buffer too small; *k holds the size needed */
+} tl_status;
+
+/* algorithm selection (trilist_cli.cpp:124-133, --algo {app,apm}) */
+enum { TL_ALGO_APP = 0, TL_ALGO_APM = 1 };
+
+/* output sinks, OR-able (the reference's --sink {count,collect}, extended) */
+enum {
+    TL_OUT_COUNT = 0,          /* CountingSink: triangle_count only */
+    TL_OUT_CHECKSUM = 1,       /* order-independent 64-bit checksum */
+    TL_OUT_VERTEX_COUNTS = 2,  /* per-vertex triangle counts, uint64[n] */
+    TL_OUT_LIST = 4            /* CollectingSink: all (u,v,w) triples */
+};
+
+typedef struct {
+    /* ListingStats (listing.hpp:23-34) */
+    uint64_t triangle_count;
+    uint64_t inner_ops; /* = c_pp (app) or c_pm (apm) */
+    uint64_t mark_ops;  /* = 2m */
+    /* extensions */
+    uint64_t checksum;  /* sum mod 2^64 of mix64 chain over dense-id-sorted triples */
+    uint64_t c_pp, c_pm, c_mm, sum_deg_sq; /* CostReport (cost.hpp:15-20) */
+    double orient_ms;   /* device time of the last tl_orient (relabel+CSR+sort) */
+    double list_ms;     /* device time of the listing kernels (ListingStats::wall_ms analogue) */
+    double h2d_ms;      /* host->device copy time of the last tl_orient (0 for _device) */
+    uint64_t kernel_launches; /* kernels launched by the last orient + list */
+} tl_stats;
+
+TL_API int tl_version(void);
+TL_API tl_status tl_create(tl_ctx** out, int device);
+TL_API void tl_destroy(tl_ctx* ctx);
+/* Last error text for ctx (or for a failed tl_create when ctx is NULL). */
+TL_API const char* tl_last_error(const tl_ctx* ctx);
+
+/* Build the oriented view on the device from HOST arrays (copied in). */
+TL_API tl_status tl_orient(tl_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* offsets,
+                           const uint32_t* adj, const uint32_t* rank);
+/* Same from DEVICE arrays owned by the caller, valid for the duration of the
+ * call (inputs already resident in HBM). */
+TL_API tl_status tl_orient_device(tl_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* d_offsets,
+                                  const uint32_t* d_adj, const uint32_t* d_rank);
+/* Mismatched sizes (rank length != n) are reported as in oriented_view.cpp:8-9. */
+TL_API tl_status tl_check_sizes(uint32_t graph_n, uint32_t rank_n);
+
+/* List every triangle once over G_pi with A++ (TL_ALGO_APP, listing.hpp:69-86)
+ * or A+- (TL_ALGO_APM, listing.hpp:91-107). */
+TL_API tl_status tl_list(tl_ctx* ctx, int algo, unsigned out_flags, tl_stats* out);
+
+/* Copy the triangles of the last TL_OUT_LIST run: 3*k dense ids, each triple
+ * rank-ascending (u, v, w), triples in unspecified order. cap in triangles.
+ * TL_ERR_CAPACITY (with *k set) when cap is too small. */
+TL_API tl_status tl_fetch_triangles(tl_ctx* ctx, uint32_t* uvw, uint64_t cap, uint64_t* k);
+/* Per-vertex triangle counts (dense ids) of the last TL_OUT_VERTEX_COUNTS run. */
+TL_API tl_status tl_fetch_vertex_counts(tl_ctx* ctx, uint64_t* counts);
+/* The oriented view in the reference layout (oriented_view.hpp:41-45):
+ * succ_off/pred_off uint64[n+1] indexed by dense id, succ/pred uint32[m]
+ * holding dense ids, each row rank-ascending. Any pointer may be NULL. */
+TL_API tl_status tl_fetch_oriented(tl_ctx* ctx, uint64_t* succ_off, uint32_t* succ,
+                                   uint64_t* pred_off, uint32_t* pred);
+/* {c_pp, c_pm, c_mm, sum_deg_sq} of the current view. */
+TL_API tl_status tl_cost_report(tl_ctx* ctx, uint64_t out[4]);
+
+/* Page-lock / unlock caller host memory so tl_orient's copies run at full
+ * PCIe rate (cudaHostRegister). */
+TL_API tl_status tl_host_register(tl_ctx* ctx, void* ptr, size_t bytes);
+TL_API tl_status tl_host_unregister(tl_ctx* ctx, void* ptr);
+
+/* Per-phase device times (ms) of the last orient + list, named by
+ * tl_phase_name(i); returns the number of phases written (<= cap). */
+TL_API int tl_phase_times(const tl_ctx* ctx, double* ms, int cap);
+TL_API const char* tl_phase_name(int i);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

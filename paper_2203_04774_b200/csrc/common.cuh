@@ -1,0 +1,70 @@
+// common.cuh -- shared device helpers for the trigpu engine (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace trigpu {
+
+constexpr unsigned FULL = 0xFFFFFFFFu;
+constexpr uint32_t kNone = 0xFFFFFFFFu;  // kInvalidVertex (common.hpp:13)
+
+// splitmix64 finaliser; identical to oracle/oracle.c:or_mix64 and to the
+// reference-harness checksum sink.
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+// Order-independent triangle hash over DENSE ids: sort the triple, then
+// mix64(mix64(mix64(a) ^ b) ^ c).
+__host__ __device__ __forceinline__ uint64_t tri_hash(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t lo = a < b ? a : b, hi = a < b ? b : a;
+    uint32_t mid;
+    if (c < lo) { mid = lo; lo = c; }
+    else if (c > hi) { mid = hi; hi = c; }
+    else mid = c;
+    return mix64(mix64(mix64(lo) ^ mid) ^ hi);
+}
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+__device__ __forceinline__ unsigned lanemask_le() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_le;" : "=r"(m));
+    return m;
+}
+
+__device__ __forceinline__ uint64_t shfl64(uint64_t v, int src) {
+    uint32_t lo = __shfl_sync(FULL, static_cast<uint32_t>(v), src);
+    uint32_t hi = __shfl_sync(FULL, static_cast<uint32_t>(v >> 32), src);
+    return (static_cast<uint64_t>(hi) << 32) | lo;
+}
+
+__device__ __forceinline__ uint64_t warp_sum64(uint64_t v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    return v;
+}
+
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
+    const unsigned lane = lane_id();
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t t = __shfl_up_sync(FULL, v, o);
+        if (lane >= static_cast<unsigned>(o)) v += t;
+    }
+    return v;
+}
+
+// Multiplicative hash into a power-of-two table of 2^bits slots.
+__device__ __forceinline__ uint32_t slot_hash(uint32_t key, uint32_t shift) {
+    return (key * 0x9E3779B1u) >> shift;  // shift = 32 - bits
+}
+
+}  // namespace trigpu

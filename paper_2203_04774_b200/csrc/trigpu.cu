@@ -1,0 +1,696 @@
+// trigpu.cu -- context, device memory and the C-ABI (include/trigpu.h).
+//
+// One tl_ctx = one device + two CUDA streams + grow-only device buffers laid
+// out for HBM residency (SURVEY §8 byte table):
+//   input graph   goff u64[n+1], gadj u32[2m]        (owned copy, tl_orient only)
+//   pi            rank u32[n], inv u32[n]
+//   relabelled    radj u32[2m]  (rank[adj[e]]; reused as the sort temp row)
+//   out-CSR       out_off u64[n+1], out_adj u32[m]   (rank space, rows ascending)
+//   in-CSR        in_off u64[n+1], in_adj u32[m]     (built on first A++ / export)
+//   degrees       outdeg u32[n], indeg u32[n]
+//   work lists    lists u32[4n] (sort classes during orient, seed classes
+//                 during listing)
+//   sinks         acc u64[8], vcount u64[n], tri u32[3T]
+// Host <-> device crossings: the input copy in tl_orient, small scalar
+// read-backs (error flags, class counts, stats) and the explicit fetches.
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+#include "listing.cuh"
+#include "orient.cuh"
+#include "segsort.cuh"
+#include "trigpu.h"
+
+using namespace trigpu;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+enum Phase {
+    PH_H2D = 0,
+    PH_RELABEL,
+    PH_SCAN,
+    PH_SCATTER,
+    PH_SORT,
+    PH_COST,
+    PH_IN_CSR,
+    PH_CLASSIFY,
+    PH_LIST,
+    PH_COUNT
+};
+const char* kPhaseNames[PH_COUNT] = {"h2d",  "relabel_count", "scan",     "scatter", "segsort",
+                                     "cost", "in_csr",        "classify", "list"};
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+};
+
+}  // namespace
+
+struct tl_ctx {
+    int device = 0;
+    int sms = 148;
+    cudaStream_t s = nullptr, s2 = nullptr;
+    cudaEvent_t ev[2 * PH_COUNT + 4] = {};
+    cudaEvent_t fork = nullptr, join = nullptr;
+    std::string err;
+    double phase_ms[PH_COUNT] = {};
+    uint64_t launches = 0;
+
+    uint32_t n = 0;
+    uint64_t m = 0;
+    bool oriented = false, in_built = false;
+    uint32_t max_out = 0;
+    unsigned long long cost[4] = {0, 0, 0, 0};
+    double h2d_ms = 0, orient_ms = 0;
+
+    DevBuf goff, gadj, rank, inv, radj, out_off, out_adj, in_off, in_adj, outdeg, indeg, lists, acc,
+        vcount, tri, scan_part, bitmaps, small;
+    bool have_vcounts = false, have_tri = false;
+    unsigned long long tri_count = 0;
+
+    tl_status fail(tl_status st, const std::string& what) {
+        err = what;
+        return st;
+    }
+    tl_status cuda_fail(const char* what, cudaError_t e) {
+        err = std::string(what) + ": " + cudaGetErrorString(e);
+        (void)cudaGetLastError();
+        return e == cudaErrorMemoryAllocation ? TL_ERR_OUT_OF_MEMORY : TL_ERR_CUDA;
+    }
+};
+
+#define CK(call)                                                  \
+    do {                                                          \
+        cudaError_t e_ = (call);                                  \
+        if (e_ != cudaSuccess) return ctx->cuda_fail(#call, e_); \
+    } while (0)
+#define LAUNCHED()                                                                  \
+    do {                                                                            \
+        ++ctx->launches;                                                            \
+        cudaError_t e_ = cudaGetLastError();                                        \
+        if (e_ != cudaSuccess) return ctx->cuda_fail("kernel launch", e_);          \
+    } while (0)
+
+namespace {
+
+tl_status ensure(tl_ctx* ctx, DevBuf& b, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    if (b.cap >= bytes) return TL_OK;
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.cap = 0;
+    cudaError_t e = cudaMalloc(&b.p, bytes);
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        return ctx->fail(TL_ERR_OUT_OF_MEMORY,
+                         "cudaMalloc of " + std::to_string(bytes) + " bytes failed: " + cudaGetErrorString(e));
+    }
+    b.cap = bytes;
+    return TL_OK;
+}
+
+#define ENSURE(buf, bytes)                                 \
+    do {                                                   \
+        tl_status st_ = ensure(ctx, ctx->buf, (bytes));    \
+        if (st_ != TL_OK) return st_;                      \
+    } while (0)
+
+template <class T>
+T* P(DevBuf& b) {
+    return static_cast<T*>(b.p);
+}
+
+unsigned grid_for(uint64_t items, unsigned threads, unsigned cap) {
+    uint64_t g = (items + threads - 1) / threads;
+    if (g < 1) g = 1;
+    return static_cast<unsigned>(std::min<uint64_t>(g, cap));
+}
+
+double ev_ms(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    return ms;
+}
+
+// offsets[0..n] = exclusive scan of cnt[0..n)
+tl_status scan_offsets(tl_ctx* ctx, uint32_t n, const uint32_t* cnt, uint64_t* off) {
+    const uint64_t tiles = std::max<uint64_t>(1, (static_cast<uint64_t>(n) + kScanTile - 1) / kScanTile);
+    ENSURE(scan_part, tiles * sizeof(unsigned long long));
+    auto* part = P<unsigned long long>(ctx->scan_part);
+    k_scan_partials<<<(unsigned)tiles, kScanThreads, 0, ctx->s>>>(n, cnt, part);
+    LAUNCHED();
+    k_scan_tops<<<1, kScanThreads, 0, ctx->s>>>(tiles, part);
+    LAUNCHED();
+    k_scan_apply<<<(unsigned)tiles, kScanThreads, 0, ctx->s>>>(n, cnt, part, off);
+    LAUNCHED();
+    return TL_OK;
+}
+
+// Segmented sort of every row of (off, adj) in place; tmp has >= off[n] slots.
+tl_status sort_rows(tl_ctx* ctx, uint32_t n, uint64_t* off, uint32_t* adj, uint32_t* tmp) {
+    ENSURE(small, 64);
+    auto* counts = static_cast<unsigned int*>(ctx->small.p);
+    CK(cudaMemsetAsync(counts, 0, 4 * sizeof(unsigned int), ctx->s));
+    uint32_t* lists = P<uint32_t>(ctx->lists);
+    SortLists L{lists, lists + n, lists + 2 * (uint64_t)n, counts};
+    k_sort_small<<<grid_for(n, 256, ctx->sms * 16), 256, 0, ctx->s>>>(n, off, adj, L);
+    LAUNCHED();
+    unsigned int h[4];
+    CK(cudaMemcpyAsync(h, counts, sizeof(h), cudaMemcpyDeviceToHost, ctx->s));
+    CK(cudaStreamSynchronize(ctx->s));
+    const int end_bit = std::min(32, (int)(32 - __builtin_clz(std::max(n, 2u) - 1)) + 1);
+    if (h[0]) {
+        k_sort_warp<<<grid_for((uint64_t)h[0] * 32, 256, ctx->sms * 8), 256, 0, ctx->s>>>(off, adj, L.warp_rows,
+                                                                                          counts + 0);
+        LAUNCHED();
+    }
+    if (h[1]) {
+        k_sort_block<<<std::min<unsigned>(h[1], ctx->sms * 8), kBlockSortThreads, 0, ctx->s>>>(
+            off, adj, L.block_rows, counts + 1, end_bit);
+        LAUNCHED();
+    }
+    if (h[2]) {
+        const size_t smem = sizeof(BigSortSmem);
+        CK(cudaFuncSetAttribute(k_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_sort_big<<<std::min<unsigned>(h[2], ctx->sms * 2), kBigThreads, smem, ctx->s>>>(n, off, adj, tmp,
+                                                                                       L.big_rows, counts + 2);
+        LAUNCHED();
+    }
+    return TL_OK;
+}
+
+tl_status orient_core(tl_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* goff, const uint32_t* gadj,
+                      const uint32_t* rank) {
+    ctx->oriented = false;
+    ctx->in_built = false;
+    ctx->have_vcounts = false;
+    ctx->have_tri = false;
+    ctx->n = n;
+    ctx->m = m;
+    ENSURE(inv, (size_t)n * 4);
+    ENSURE(radj, 2 * m * 4);
+    ENSURE(outdeg, (size_t)n * 4);
+    ENSURE(indeg, (size_t)n * 4);
+    ENSURE(out_off, ((size_t)n + 1) * 8);
+    ENSURE(out_adj, m * 4);
+    ENSURE(lists, (size_t)n * 16);
+    ENSURE(small, 64);
+    auto* flags = static_cast<unsigned long long*>(ctx->small.p);  // [0] err, [4..] scratch
+    const unsigned big = ctx->sms * 16;
+
+    CK(cudaMemsetAsync(ctx->inv.p, 0xFF, (size_t)n * 4, ctx->s));
+    CK(cudaMemsetAsync(flags, 0, 64, ctx->s));
+    if (n) {
+        k_inverse<<<grid_for(n, 256, big), 256, 0, ctx->s>>>(n, rank, P<uint32_t>(ctx->inv), flags);
+        LAUNCHED();
+        k_relabel_count<<<grid_for((uint64_t)n * 32, 256, big * 2), 256, 0, ctx->s>>>(
+            n, goff, gadj, rank, P<uint32_t>(ctx->radj), P<uint32_t>(ctx->outdeg), P<uint32_t>(ctx->indeg), flags);
+        LAUNCHED();
+    }
+    CK(cudaEventRecord(ctx->ev[PH_RELABEL], ctx->s));
+    unsigned long long errflag = 0;
+    CK(cudaMemcpyAsync(&errflag, flags, 8, cudaMemcpyDeviceToHost, ctx->s));
+    CK(cudaStreamSynchronize(ctx->s));
+    if (errflag & 3ull) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "orient: ordering does not match graph (rank is not a permutation of [0, n))");
+    if (errflag & 4ull) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "orient: adjacency violates the Graph invariants (rows must be strictly increasing, in range, loop-free)");
+
+    tl_status st = scan_offsets(ctx, n, P<uint32_t>(ctx->outdeg), P<uint64_t>(ctx->out_off));
+    if (st != TL_OK) return st;
+    CK(cudaEventRecord(ctx->ev[PH_SCAN], ctx->s));
+    if (n) {
+        k_scatter<false><<<grid_for((uint64_t)n * 32, 256, big * 2), 256, 0, ctx->s>>>(
+            n, goff, P<uint32_t>(ctx->radj), rank, P<uint64_t>(ctx->out_off), P<uint32_t>(ctx->out_adj), nullptr,
+            nullptr);
+        LAUNCHED();
+    }
+    CK(cudaEventRecord(ctx->ev[PH_SCATTER], ctx->s));
+    st = sort_rows(ctx, n, P<uint64_t>(ctx->out_off), P<uint32_t>(ctx->out_adj), P<uint32_t>(ctx->radj));
+    if (st != TL_OK) return st;
+    CK(cudaEventRecord(ctx->ev[PH_SORT], ctx->s));
+    // costs + max out-degree
+    CK(cudaMemsetAsync(flags + 2, 0, 5 * 8, ctx->s));
+    if (n) {
+        k_cost<<<grid_for(n, 256, ctx->sms * 4), 256, 0, ctx->s>>>(n, P<uint32_t>(ctx->outdeg), P<uint32_t>(ctx->indeg),
+                                                                  flags + 2);
+        LAUNCHED();
+        k_maxdeg<<<grid_for(n, 256, ctx->sms * 4), 256, 0, ctx->s>>>(n, P<uint32_t>(ctx->outdeg),
+                                                                    reinterpret_cast<unsigned int*>(flags + 6));
+        LAUNCHED();
+    }
+    CK(cudaEventRecord(ctx->ev[PH_COST], ctx->s));
+    unsigned long long res[5];
+    CK(cudaMemcpyAsync(res, flags + 2, sizeof(res), cudaMemcpyDeviceToHost, ctx->s));
+    CK(cudaStreamSynchronize(ctx->s));
+    std::memcpy(ctx->cost, res, sizeof(ctx->cost));
+    ctx->max_out = static_cast<uint32_t>(res[4]);
+    ctx->phase_ms[PH_RELABEL] = ev_ms(ctx->ev[PH_H2D], ctx->ev[PH_RELABEL]);
+    ctx->phase_ms[PH_SCAN] = ev_ms(ctx->ev[PH_RELABEL], ctx->ev[PH_SCAN]);
+    ctx->phase_ms[PH_SCATTER] = ev_ms(ctx->ev[PH_SCAN], ctx->ev[PH_SCATTER]);
+    ctx->phase_ms[PH_SORT] = ev_ms(ctx->ev[PH_SCATTER], ctx->ev[PH_SORT]);
+    ctx->phase_ms[PH_COST] = ev_ms(ctx->ev[PH_SORT], ctx->ev[PH_COST]);
+    ctx->orient_ms = ev_ms(ctx->ev[PH_H2D], ctx->ev[PH_COST]);
+    ctx->oriented = true;
+    return TL_OK;
+}
+
+// k_transpose: in-row s receives r for every successor s of r.
+__global__ void k_transpose(uint32_t n, const uint64_t* __restrict__ out_off, const uint32_t* __restrict__ out_adj,
+                            unsigned long long* __restrict__ cursor, uint32_t* __restrict__ in_adj) {
+    const unsigned lane = lane_id();
+    const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t r = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; r < n; r += warps) {
+        const uint64_t b = out_off[r], e = out_off[r + 1];
+        for (uint64_t i = b + lane; i < e; i += 32) {
+            const uint32_t s = out_adj[i];
+            in_adj[atomicAdd(&cursor[s], 1ull)] = static_cast<uint32_t>(r);
+        }
+    }
+}
+
+// In-CSR (predecessor rows) by transposing the out-CSR, then the same
+// segmented sort. Built lazily: A+- never needs it.
+tl_status ensure_in_csr(tl_ctx* ctx) {
+    if (ctx->in_built) return TL_OK;
+    const uint32_t n = ctx->n;
+    const uint64_t m = ctx->m;
+    ENSURE(in_off, ((size_t)n + 1) * 8);
+    ENSURE(in_adj, m * 4);
+    CK(cudaEventRecord(ctx->ev[PH_COUNT + 0], ctx->s));
+    tl_status st = scan_offsets(ctx, n, P<uint32_t>(ctx->indeg), P<uint64_t>(ctx->in_off));
+    if (st != TL_OK) return st;
+    // cursor = copy of in_off (radj is free after orientation; 2m u32 = m u64)
+    auto* cursor = P<unsigned long long>(ctx->radj);
+    if (n) {
+        CK(cudaMemcpyAsync(cursor, ctx->in_off.p, (size_t)n * 8, cudaMemcpyDeviceToDevice, ctx->s));
+        k_transpose<<<grid_for((uint64_t)n * 32, 256, ctx->sms * 32), 256, 0, ctx->s>>>(
+            n, P<uint64_t>(ctx->out_off), P<uint32_t>(ctx->out_adj), cursor, P<uint32_t>(ctx->in_adj));
+        LAUNCHED();
+    }
+    st = sort_rows(ctx, n, P<uint64_t>(ctx->in_off), P<uint32_t>(ctx->in_adj), P<uint32_t>(ctx->radj));
+    if (st != TL_OK) return st;
+    CK(cudaEventRecord(ctx->ev[PH_COUNT + 1], ctx->s));
+    CK(cudaStreamSynchronize(ctx->s));
+    ctx->phase_ms[PH_IN_CSR] = ev_ms(ctx->ev[PH_COUNT + 0], ctx->ev[PH_COUNT + 1]);
+    ctx->in_built = true;
+    return TL_OK;
+}
+
+template <int ALGO, unsigned F>
+tl_status launch_classes(tl_ctx* ctx, ListParams base, uint32_t* const lists[4], const unsigned h[4],
+                         unsigned int* queues) {
+    const int sms = ctx->sms;
+    // class G first, on the side stream: a few long CTAs overlap the rest
+    if (h[3]) {
+        ListParams p = base;
+        p.seeds = lists[3];
+        p.nseeds = h[3];
+        p.queue = queues + 3;
+        const unsigned grid = std::min<unsigned>(h[3], (unsigned)sms);
+        p.bitmap_words = ((uint64_t)ctx->n + 31) / 32 + 32;
+        ENSURE(bitmaps, (size_t)grid * p.bitmap_words * 4);
+        p.bitmaps = P<uint32_t>(ctx->bitmaps);
+        CK(cudaEventRecord(ctx->fork, ctx->s));
+        CK(cudaStreamWaitEvent(ctx->s2, ctx->fork, 0));
+        k_list_giant<ALGO, F><<<grid, kGThreads, 0, ctx->s2>>>(p);
+        LAUNCHED();
+        CK(cudaEventRecord(ctx->join, ctx->s2));
+    }
+    if (h[0]) {
+        ListParams p = base;
+        p.seeds = lists[0];
+        p.nseeds = h[0];
+        p.queue = queues + 0;
+        k_list_reg<ALGO, F><<<grid_for((uint64_t)h[0] * 32, 256, sms * 8), 256, 0, ctx->s>>>(p);
+        LAUNCHED();
+    }
+    if (h[1]) {
+        ListParams p = base;
+        p.seeds = lists[1];
+        p.nseeds = h[1];
+        p.queue = queues + 1;
+        k_list_hash_warp<ALGO, F><<<grid_for((uint64_t)h[1] * 32, kHWarps * 32, sms * 6), kHWarps * 32, 0, ctx->s>>>(p);
+        LAUNCHED();
+    }
+    if (h[2]) {
+        ListParams p = base;
+        p.seeds = lists[2];
+        p.nseeds = h[2];
+        p.queue = queues + 2;
+        const size_t smem = (1u << kCMaxBits) * 4;
+        CK(cudaFuncSetAttribute(k_list_hash_cta<ALGO, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_list_hash_cta<ALGO, F><<<std::min<unsigned>(h[2] * kCMaxSlices, sms * 3), kCThreads, smem, ctx->s>>>(p);
+        LAUNCHED();
+    }
+    if (h[3]) CK(cudaStreamWaitEvent(ctx->s, ctx->join, 0));
+    return TL_OK;
+}
+
+template <int ALGO>
+tl_status launch_flags(tl_ctx* ctx, unsigned F, ListParams base, uint32_t* const lists[4], const unsigned h[4],
+                       unsigned int* queues) {
+    switch (F & 7u) {
+        case 0: return launch_classes<ALGO, 0>(ctx, base, lists, h, queues);
+        case 1: return launch_classes<ALGO, 1>(ctx, base, lists, h, queues);
+        case 2: return launch_classes<ALGO, 2>(ctx, base, lists, h, queues);
+        case 3: return launch_classes<ALGO, 3>(ctx, base, lists, h, queues);
+        case 4: return launch_classes<ALGO, 4>(ctx, base, lists, h, queues);
+        case 5: return launch_classes<ALGO, 5>(ctx, base, lists, h, queues);
+        case 6: return launch_classes<ALGO, 6>(ctx, base, lists, h, queues);
+        default: return launch_classes<ALGO, 7>(ctx, base, lists, h, queues);
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+TL_API int tl_version(void) { return 1; }
+
+TL_API tl_status tl_create(tl_ctx** out, int device) {
+    if (!out) return TL_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0) {
+        (void)cudaGetLastError();
+        g_create_error = std::string("tl_create: no CUDA device available (") +
+                         (e != cudaSuccess ? cudaGetErrorString(e) : "device count 0") + ")";
+        return TL_ERR_CUDA;
+    }
+    if (device < 0 || device >= count) {
+        g_create_error = "tl_create: device index out of range";
+        return TL_ERR_INVALID_ARGUMENT;
+    }
+    cudaDeviceProp prop;
+    if ((e = cudaGetDeviceProperties(&prop, device)) != cudaSuccess || prop.major < 10) {
+        g_create_error = e != cudaSuccess ? std::string("tl_create: ") + cudaGetErrorString(e)
+                                          : "tl_create: this engine is built for sm_100a (B200) only";
+        return TL_ERR_CUDA;
+    }
+    tl_ctx* ctx = new tl_ctx();
+    ctx->device = device;
+    ctx->sms = prop.multiProcessorCount;
+    if ((e = cudaSetDevice(device)) != cudaSuccess || (e = cudaStreamCreateWithFlags(&ctx->s, cudaStreamNonBlocking)) != cudaSuccess ||
+        (e = cudaStreamCreateWithFlags(&ctx->s2, cudaStreamNonBlocking)) != cudaSuccess) {
+        g_create_error = std::string("tl_create: ") + cudaGetErrorString(e);
+        delete ctx;
+        return TL_ERR_CUDA;
+    }
+    for (auto& ev : ctx->ev) cudaEventCreate(&ev);
+    cudaEventCreateWithFlags(&ctx->fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ctx->join, cudaEventDisableTiming);
+    *out = ctx;
+    return TL_OK;
+}
+
+TL_API void tl_destroy(tl_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->s);
+    cudaStreamSynchronize(ctx->s2);
+    DevBuf* bufs[] = {&ctx->goff,   &ctx->gadj,   &ctx->rank,  &ctx->inv,    &ctx->radj,      &ctx->out_off,
+                      &ctx->out_adj, &ctx->in_off, &ctx->in_adj, &ctx->outdeg, &ctx->indeg,     &ctx->lists,
+                      &ctx->acc,    &ctx->vcount, &ctx->tri,   &ctx->scan_part, &ctx->bitmaps, &ctx->small};
+    for (DevBuf* b : bufs)
+        if (b->p) cudaFree(b->p);
+    for (auto& ev : ctx->ev) cudaEventDestroy(ev);
+    cudaEventDestroy(ctx->fork);
+    cudaEventDestroy(ctx->join);
+    cudaStreamDestroy(ctx->s);
+    cudaStreamDestroy(ctx->s2);
+    delete ctx;
+}
+
+TL_API const char* tl_last_error(const tl_ctx* ctx) {
+    return ctx ? ctx->err.c_str() : g_create_error.c_str();
+}
+
+TL_API tl_status tl_check_sizes(uint32_t graph_n, uint32_t rank_n) {
+    return graph_n == rank_n ? TL_OK : TL_ERR_INVALID_ARGUMENT;
+}
+
+static tl_status check_args(tl_ctx* ctx, uint32_t n, uint64_t m, const void* off, const void* adj, const void* rank) {
+    if (!ctx) return TL_ERR_INVALID_ARGUMENT;
+    ctx->launches = 0;
+    if ((n && (!off || !rank)) || (m && !adj)) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "orient: null input pointer");
+    if (n == 0xFFFFFFFFu) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "orient: n must be < 2^32 - 1 (VertexId, common.hpp:11-13)");
+    if (m > (uint64_t)n * (n ? n - 1 : 0) / 2) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "orient: m exceeds n(n-1)/2");
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return ctx->cuda_fail("cudaSetDevice", cudaGetLastError());
+    return TL_OK;
+}
+
+TL_API tl_status tl_orient(tl_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* offsets, const uint32_t* adj,
+                           const uint32_t* rank) {
+    tl_status st = check_args(ctx, n, m, offsets, adj, rank);
+    if (st != TL_OK) return st;
+    if (n && offsets[0] != 0) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "orient: offsets[0] must be 0");
+    if (n && offsets[n] != 2 * m) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "orient: offsets[n] must equal 2m");
+    ENSURE(goff, ((size_t)n + 1) * 8);
+    ENSURE(gadj, 2 * m * 4);
+    ENSURE(rank, (size_t)n * 4);
+    CK(cudaEventRecord(ctx->ev[PH_COUNT + 2], ctx->s));
+    CK(cudaMemcpyAsync(ctx->goff.p, offsets, ((size_t)n + 1) * 8, cudaMemcpyHostToDevice, ctx->s));
+    if (m) CK(cudaMemcpyAsync(ctx->gadj.p, adj, 2 * m * 4, cudaMemcpyHostToDevice, ctx->s));
+    if (n) CK(cudaMemcpyAsync(ctx->rank.p, rank, (size_t)n * 4, cudaMemcpyHostToDevice, ctx->s));
+    CK(cudaEventRecord(ctx->ev[PH_H2D], ctx->s));
+    st = orient_core(ctx, n, m, P<uint64_t>(ctx->goff), P<uint32_t>(ctx->gadj), P<uint32_t>(ctx->rank));
+    if (st != TL_OK) return st;
+    ctx->h2d_ms = ctx->phase_ms[PH_H2D] = ev_ms(ctx->ev[PH_COUNT + 2], ctx->ev[PH_H2D]);
+    return TL_OK;
+}
+
+TL_API tl_status tl_orient_device(tl_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* d_offsets,
+                                  const uint32_t* d_adj, const uint32_t* d_rank) {
+    tl_status st = check_args(ctx, n, m, d_offsets, d_adj, d_rank);
+    if (st != TL_OK) return st;
+    // keep pi: exports map ranks back to dense ids after the call returns
+    ENSURE(rank, (size_t)n * 4);
+    CK(cudaEventRecord(ctx->ev[PH_H2D], ctx->s));
+    if (n) CK(cudaMemcpyAsync(ctx->rank.p, d_rank, (size_t)n * 4, cudaMemcpyDeviceToDevice, ctx->s));
+    st = orient_core(ctx, n, m, d_offsets, d_adj, P<uint32_t>(ctx->rank));
+    if (st != TL_OK) return st;
+    ctx->h2d_ms = ctx->phase_ms[PH_H2D] = 0;
+    return TL_OK;
+}
+
+TL_API tl_status tl_list(tl_ctx* ctx, int algo, unsigned out_flags, tl_stats* out) {
+    if (!ctx) return TL_ERR_INVALID_ARGUMENT;
+    if (!ctx->oriented) return ctx->fail(TL_ERR_STATE, "tl_list: no oriented view (call tl_orient first)");
+    if (algo != TL_ALGO_APP && algo != TL_ALGO_APM) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "tl_list: algo must be TL_ALGO_APP or TL_ALGO_APM");
+    if (out_flags & ~7u) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "tl_list: unknown output flag");
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return ctx->cuda_fail("cudaSetDevice", cudaGetLastError());
+    if ((uint64_t)ctx->max_out * 32 >= (1ull << 32))
+        return ctx->fail(TL_ERR_INVALID_ARGUMENT, "tl_list: out-degree >= 2^27 is not supported");
+    const uint32_t n = ctx->n;
+    tl_status st;
+    if (algo == TL_ALGO_APP) {
+        st = ensure_in_csr(ctx);
+        if (st != TL_OK) return st;
+    }
+    ENSURE(acc, 8 * sizeof(unsigned long long));
+    ENSURE(small, 64);
+    auto* acc = P<unsigned long long>(ctx->acc);
+    auto* counts = static_cast<unsigned int*>(ctx->small.p);  // [0..3] class sizes, [4..7] queues
+    const bool want_vc = out_flags & TL_OUT_VERTEX_COUNTS;
+    const bool want_list = out_flags & TL_OUT_LIST;
+    if (want_vc) ENSURE(vcount, (size_t)n * 8);
+
+    ListParams base{};
+    base.n = n;
+    base.set_off = algo == TL_ALGO_APM ? P<uint64_t>(ctx->out_off) : P<uint64_t>(ctx->in_off);
+    base.set_adj = algo == TL_ALGO_APM ? P<uint32_t>(ctx->out_adj) : P<uint32_t>(ctx->in_adj);
+    base.out_off = P<uint64_t>(ctx->out_off);
+    base.out_adj = P<uint32_t>(ctx->out_adj);
+    base.inv = P<uint32_t>(ctx->inv);
+    base.acc = acc;
+    base.vcount = want_vc ? P<unsigned long long>(ctx->vcount) : nullptr;
+
+    CK(cudaEventRecord(ctx->ev[PH_COUNT + 3], ctx->s));
+    CK(cudaMemsetAsync(counts, 0, 8 * sizeof(unsigned int), ctx->s));
+    uint32_t* L = P<uint32_t>(ctx->lists);
+    uint32_t* const lists[4] = {L, L + n, L + 2 * (uint64_t)n, L + 3 * (uint64_t)n};
+    SeedLists SL{{lists[0], lists[1], lists[2], lists[3]}, counts};
+    if (n) {
+        k_classify_seeds<<<grid_for(n, 256, ctx->sms * 16), 256, 0, ctx->s>>>(n, base.set_off, SL);
+        LAUNCHED();
+    }
+    CK(cudaEventRecord(ctx->ev[PH_CLASSIFY], ctx->s));
+    unsigned h[4];
+    CK(cudaMemcpyAsync(h, counts, sizeof(h), cudaMemcpyDeviceToHost, ctx->s));
+    CK(cudaStreamSynchronize(ctx->s));
+
+    auto run = [&](unsigned F) -> tl_status {
+        CK(cudaMemsetAsync(acc, 0, 8 * sizeof(unsigned long long), ctx->s));
+        CK(cudaMemsetAsync(counts + 4, 0, 4 * sizeof(unsigned int), ctx->s));
+        if (F & F_VCOUNT) CK(cudaMemsetAsync(ctx->vcount.p, 0, (size_t)n * 8, ctx->s));
+        return algo == TL_ALGO_APM ? launch_flags<ALGO_APM>(ctx, F, base, lists, h, counts + 4)
+                                   : launch_flags<ALGO_APP>(ctx, F, base, lists, h, counts + 4);
+    };
+    unsigned long long res[3] = {0, 0, 0};
+    if (want_list) {
+        // pass 1 counts, so the triangle buffer is sized exactly
+        st = run(0);
+        if (st != TL_OK) return st;
+        CK(cudaMemcpyAsync(res, acc, 8, cudaMemcpyDeviceToHost, ctx->s));
+        CK(cudaStreamSynchronize(ctx->s));
+        ENSURE(tri, (size_t)std::max<unsigned long long>(res[0], 1) * 12);
+        base.tri = P<uint32_t>(ctx->tri);
+        base.tri_cap = res[0];
+    }
+    st = run(out_flags);
+    if (st != TL_OK) return st;
+    CK(cudaEventRecord(ctx->ev[PH_LIST], ctx->s));
+    CK(cudaMemcpyAsync(res, acc, sizeof(res), cudaMemcpyDeviceToHost, ctx->s));
+    CK(cudaStreamSynchronize(ctx->s));
+    ctx->phase_ms[PH_CLASSIFY] = ev_ms(ctx->ev[PH_COUNT + 3], ctx->ev[PH_CLASSIFY]);
+    ctx->phase_ms[PH_LIST] = ev_ms(ctx->ev[PH_CLASSIFY], ctx->ev[PH_LIST]);
+    ctx->have_vcounts = want_vc;
+    ctx->have_tri = want_list;
+    ctx->tri_count = want_list ? res[2] : 0;
+    if (want_list && res[2] != res[0])
+        return ctx->fail(TL_ERR_CUDA, "tl_list: list pass emitted a different number of triangles than the count pass");
+    if (out) {
+        std::memset(out, 0, sizeof(*out));
+        out->triangle_count = res[0];
+        out->checksum = (out_flags & TL_OUT_CHECKSUM) ? res[1] : 0;
+        out->c_pp = ctx->cost[0];
+        out->c_pm = ctx->cost[1];
+        out->c_mm = ctx->cost[2];
+        out->sum_deg_sq = ctx->cost[3];
+        out->inner_ops = algo == TL_ALGO_APM ? ctx->cost[1] : ctx->cost[0];
+        out->mark_ops = 2 * ctx->m;
+        out->orient_ms = ctx->orient_ms;
+        out->list_ms = ev_ms(ctx->ev[PH_COUNT + 3], ctx->ev[PH_LIST]);
+        out->h2d_ms = ctx->h2d_ms;
+        out->kernel_launches = ctx->launches;
+    }
+    return TL_OK;
+}
+
+TL_API tl_status tl_fetch_triangles(tl_ctx* ctx, uint32_t* uvw, uint64_t cap, uint64_t* k) {
+    if (!ctx || !k) return TL_ERR_INVALID_ARGUMENT;
+    if (!ctx->have_tri) return ctx->fail(TL_ERR_STATE, "tl_fetch_triangles: last tl_list did not use TL_OUT_LIST");
+    *k = ctx->tri_count;
+    if (cap < ctx->tri_count) return ctx->fail(TL_ERR_CAPACITY, "tl_fetch_triangles: buffer too small");
+    if (ctx->tri_count) {
+        if (!uvw) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "tl_fetch_triangles: null buffer");
+        CK(cudaMemcpyAsync(uvw, ctx->tri.p, ctx->tri_count * 12, cudaMemcpyDeviceToHost, ctx->s));
+        CK(cudaStreamSynchronize(ctx->s));
+    }
+    return TL_OK;
+}
+
+TL_API tl_status tl_fetch_vertex_counts(tl_ctx* ctx, uint64_t* counts) {
+    if (!ctx) return TL_ERR_INVALID_ARGUMENT;
+    if (!ctx->have_vcounts) return ctx->fail(TL_ERR_STATE, "tl_fetch_vertex_counts: last tl_list did not use TL_OUT_VERTEX_COUNTS");
+    const uint32_t n = ctx->n;
+    if (!n) return TL_OK;
+    if (!counts) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "tl_fetch_vertex_counts: null buffer");
+    // dense[u] = vcount[rank[u]]; staged through radj (>= 8n bytes not guaranteed) -> scan_part
+    ENSURE(scan_part, (size_t)n * 8);
+    k_gather_u64<<<grid_for(n, 256, ctx->sms * 16), 256, 0, ctx->s>>>(
+        n, P<unsigned long long>(ctx->vcount), P<uint32_t>(ctx->rank), P<unsigned long long>(ctx->scan_part));
+    LAUNCHED();
+    CK(cudaMemcpyAsync(counts, ctx->scan_part.p, (size_t)n * 8, cudaMemcpyDeviceToHost, ctx->s));
+    CK(cudaStreamSynchronize(ctx->s));
+    return TL_OK;
+}
+
+TL_API tl_status tl_fetch_oriented(tl_ctx* ctx, uint64_t* succ_off, uint32_t* succ, uint64_t* pred_off,
+                                   uint32_t* pred) {
+    if (!ctx) return TL_ERR_INVALID_ARGUMENT;
+    if (!ctx->oriented) return ctx->fail(TL_ERR_STATE, "tl_fetch_oriented: no oriented view");
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return ctx->cuda_fail("cudaSetDevice", cudaGetLastError());
+    const uint32_t n = ctx->n;
+    const uint64_t m = ctx->m;
+    if (pred_off || pred) {
+        tl_status st = ensure_in_csr(ctx);
+        if (st != TL_OK) return st;
+    }
+    DevBuf doff, dadj, ddeg;
+    auto cleanup = [&] {
+        if (doff.p) cudaFree(doff.p);
+        if (dadj.p) cudaFree(dadj.p);
+        if (ddeg.p) cudaFree(ddeg.p);
+    };
+    for (int side = 0; side < 2; ++side) {
+        uint64_t* ho = side == 0 ? succ_off : pred_off;
+        uint32_t* ha = side == 0 ? succ : pred;
+        if (!ho && !ha) continue;
+        tl_status st;
+        if ((st = ensure(ctx, doff, ((size_t)n + 1) * 8)) != TL_OK || (st = ensure(ctx, dadj, m * 4)) != TL_OK ||
+            (st = ensure(ctx, ddeg, (size_t)n * 4 + 4)) != TL_OK) {
+            cleanup();
+            return st;
+        }
+        const uint32_t* deg = side == 0 ? P<uint32_t>(ctx->outdeg) : P<uint32_t>(ctx->indeg);
+        const uint64_t* roff = side == 0 ? P<uint64_t>(ctx->out_off) : P<uint64_t>(ctx->in_off);
+        const uint32_t* radj = side == 0 ? P<uint32_t>(ctx->out_adj) : P<uint32_t>(ctx->in_adj);
+        if (n) {
+            k_gather_u32<<<grid_for(n, 256, ctx->sms * 16), 256, 0, ctx->s>>>(n, deg, P<uint32_t>(ctx->rank),
+                                                                            P<uint32_t>(ddeg));
+            ++ctx->launches;
+        }
+        st = scan_offsets(ctx, n, P<uint32_t>(ddeg), P<uint64_t>(doff));
+        if (st != TL_OK) {
+            cleanup();
+            return st;
+        }
+        if (n) {
+            k_export_rows<<<grid_for((uint64_t)n * 32, 256, ctx->sms * 32), 256, 0, ctx->s>>>(
+                n, P<uint32_t>(ctx->rank), P<uint32_t>(ctx->inv), roff, radj, P<uint64_t>(doff), P<uint32_t>(dadj));
+            ++ctx->launches;
+        }
+        cudaError_t e = cudaGetLastError();
+        if (e == cudaSuccess && ho) e = cudaMemcpyAsync(ho, doff.p, ((size_t)n + 1) * 8, cudaMemcpyDeviceToHost, ctx->s);
+        if (e == cudaSuccess && ha && m) e = cudaMemcpyAsync(ha, dadj.p, m * 4, cudaMemcpyDeviceToHost, ctx->s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->s);
+        if (e != cudaSuccess) {
+            cleanup();
+            return ctx->cuda_fail("tl_fetch_oriented", e);
+        }
+    }
+    cleanup();
+    return TL_OK;
+}
+
+TL_API tl_status tl_cost_report(tl_ctx* ctx, uint64_t out[4]) {
+    if (!ctx || !out) return TL_ERR_INVALID_ARGUMENT;
+    if (!ctx->oriented) return ctx->fail(TL_ERR_STATE, "tl_cost_report: no oriented view");
+    for (int i = 0; i < 4; ++i) out[i] = ctx->cost[i];
+    return TL_OK;
+}
+
+TL_API tl_status tl_host_register(tl_ctx* ctx, void* ptr, size_t bytes) {
+    if (!ctx || !ptr) return TL_ERR_INVALID_ARGUMENT;
+    cudaSetDevice(ctx->device);
+    CK(cudaHostRegister(ptr, bytes, cudaHostRegisterDefault));
+    return TL_OK;
+}
+
+TL_API tl_status tl_host_unregister(tl_ctx* ctx, void* ptr) {
+    if (!ctx || !ptr) return TL_ERR_INVALID_ARGUMENT;
+    cudaSetDevice(ctx->device);
+    CK(cudaHostUnregister(ptr));
+    return TL_OK;
+}
+
+TL_API int tl_phase_times(const tl_ctx* ctx, double* ms, int cap) {
+    if (!ctx || !ms) return 0;
+    const int k = std::min<int>(cap, PH_COUNT);
+    for (int i = 0; i < k; ++i) ms[i] = ctx->phase_ms[i];
+    return k;
+}
+
+TL_API const char* tl_phase_name(int i) { return (i >= 0 && i < PH_COUNT) ? kPhaseNames[i] : ""; }
+
+}  // extern "C"
