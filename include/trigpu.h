@@ -118,6 +118,12 @@ TL_API tl_status tl_cost_report(tl_ctx* ctx, uint64_t out[4]);
 TL_API tl_status tl_host_register(tl_ctx* ctx, void* ptr, size_t bytes);
 TL_API tl_status tl_host_unregister(tl_ctx* ctx, void* ptr);
 
+/* Device-time span on the context's stream: tl_timer_stop waits for the
+ * stream and returns the CUDA-event elapsed time since tl_timer_start
+ * (includes every kernel, copy and idle gap of the calls in between). */
+TL_API tl_status tl_timer_start(tl_ctx* ctx);
+TL_API tl_status tl_timer_stop(tl_ctx* ctx, double* ms);
+
 /* Per-phase device times (ms) of the last orient + list, named by
  * tl_phase_name(i); returns the number of phases written (<= cap). */
 TL_API int tl_phase_times(const tl_ctx* ctx, double* ms, int cap);

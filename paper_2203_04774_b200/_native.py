@@ -39,6 +39,7 @@ TRIGPU_SYMBOLS = (
     "tl_orient_device", "tl_check_sizes", "tl_list", "tl_fetch_triangles",
     "tl_fetch_vertex_counts", "tl_fetch_oriented", "tl_cost_report",
     "tl_host_register", "tl_host_unregister", "tl_phase_times", "tl_phase_name",
+    "tl_timer_start", "tl_timer_stop",
 )
 
 
@@ -111,6 +112,10 @@ def trigpu() -> C.CDLL:
     lib.tl_host_register.restype = C.c_int
     lib.tl_host_unregister.argtypes = [_vp, _vp]
     lib.tl_host_unregister.restype = C.c_int
+    lib.tl_timer_start.argtypes = [_vp]
+    lib.tl_timer_start.restype = C.c_int
+    lib.tl_timer_stop.argtypes = [_vp, C.POINTER(C.c_double)]
+    lib.tl_timer_stop.restype = C.c_int
     lib.tl_phase_times.argtypes = [_vp, C.POINTER(C.c_double), C.c_int]
     lib.tl_phase_times.restype = C.c_int
     lib.tl_phase_name.argtypes = [C.c_int]

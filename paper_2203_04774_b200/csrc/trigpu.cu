@@ -59,7 +59,8 @@ struct tl_ctx {
     int device = 0;
     int sms = 148;
     cudaStream_t s = nullptr, s2 = nullptr;
-    cudaEvent_t ev[2 * PH_COUNT + 4] = {};
+    cudaEvent_t ev[2 * PH_COUNT + 8] = {};
+    cudaEvent_t timer0 = nullptr, timer1 = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
     std::string err;
     double phase_ms[PH_COUNT] = {};
@@ -287,7 +288,9 @@ tl_status ensure_in_csr(tl_ctx* ctx) {
     CK(cudaEventRecord(ctx->ev[PH_COUNT + 0], ctx->s));
     tl_status st = scan_offsets(ctx, n, P<uint32_t>(ctx->indeg), P<uint64_t>(ctx->in_off));
     if (st != TL_OK) return st;
-    // cursor = copy of in_off (radj is free after orientation; 2m u32 = m u64)
+    // cursor = copy of in_off; radj is free after orientation (it becomes the
+    // cursor array here and the sort temp row afterwards)
+    ENSURE(radj, std::max<size_t>(2 * m * 4, (size_t)n * 8));
     auto* cursor = P<unsigned long long>(ctx->radj);
     if (n) {
         CK(cudaMemcpyAsync(cursor, ctx->in_off.p, (size_t)n * 8, cudaMemcpyDeviceToDevice, ctx->s));
@@ -316,7 +319,12 @@ tl_status launch_classes(tl_ctx* ctx, ListParams base, uint32_t* const lists[4],
         p.queue = queues + 3;
         const unsigned grid = std::min<unsigned>(h[3], (unsigned)sms);
         p.bitmap_words = ((uint64_t)ctx->n + 31) / 32 + 32;
-        ENSURE(bitmaps, (size_t)grid * p.bitmap_words * 4);
+        const size_t bm_bytes = (size_t)grid * p.bitmap_words * 4;
+        if (ctx->bitmaps.cap < bm_bytes) {
+            // fresh bitmaps start zeroed; every seed clears its own bits after use
+            ENSURE(bitmaps, bm_bytes);
+            CK(cudaMemsetAsync(ctx->bitmaps.p, 0, ctx->bitmaps.cap, ctx->s));
+        }
         p.bitmaps = P<uint32_t>(ctx->bitmaps);
         CK(cudaEventRecord(ctx->fork, ctx->s));
         CK(cudaStreamWaitEvent(ctx->s2, ctx->fork, 0));
@@ -423,6 +431,8 @@ TL_API void tl_destroy(tl_ctx* ctx) {
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     for (auto& ev : ctx->ev) cudaEventDestroy(ev);
+    if (ctx->timer0) cudaEventDestroy(ctx->timer0);
+    if (ctx->timer1) cudaEventDestroy(ctx->timer1);
     cudaEventDestroy(ctx->fork);
     cudaEventDestroy(ctx->join);
     cudaStreamDestroy(ctx->s);
@@ -528,6 +538,7 @@ TL_API tl_status tl_list(tl_ctx* ctx, int algo, unsigned out_flags, tl_stats* ou
     CK(cudaMemcpyAsync(h, counts, sizeof(h), cudaMemcpyDeviceToHost, ctx->s));
     CK(cudaStreamSynchronize(ctx->s));
 
+    CK(cudaEventRecord(ctx->ev[PH_COUNT + 4], ctx->s));  // listing kernels start
     auto run = [&](unsigned F) -> tl_status {
         CK(cudaMemsetAsync(acc, 0, 8 * sizeof(unsigned long long), ctx->s));
         CK(cudaMemsetAsync(counts + 4, 0, 4 * sizeof(unsigned int), ctx->s));
@@ -552,7 +563,7 @@ TL_API tl_status tl_list(tl_ctx* ctx, int algo, unsigned out_flags, tl_stats* ou
     CK(cudaMemcpyAsync(res, acc, sizeof(res), cudaMemcpyDeviceToHost, ctx->s));
     CK(cudaStreamSynchronize(ctx->s));
     ctx->phase_ms[PH_CLASSIFY] = ev_ms(ctx->ev[PH_COUNT + 3], ctx->ev[PH_CLASSIFY]);
-    ctx->phase_ms[PH_LIST] = ev_ms(ctx->ev[PH_CLASSIFY], ctx->ev[PH_LIST]);
+    ctx->phase_ms[PH_LIST] = ev_ms(ctx->ev[PH_COUNT + 4], ctx->ev[PH_LIST]);
     ctx->have_vcounts = want_vc;
     ctx->have_tri = want_list;
     ctx->tri_count = want_list ? res[2] : 0;
@@ -681,6 +692,26 @@ TL_API tl_status tl_host_unregister(tl_ctx* ctx, void* ptr) {
     if (!ctx || !ptr) return TL_ERR_INVALID_ARGUMENT;
     cudaSetDevice(ctx->device);
     CK(cudaHostUnregister(ptr));
+    return TL_OK;
+}
+
+TL_API tl_status tl_timer_start(tl_ctx* ctx) {
+    if (!ctx) return TL_ERR_INVALID_ARGUMENT;
+    if (!ctx->timer0) {
+        CK(cudaEventCreate(&ctx->timer0));
+        CK(cudaEventCreate(&ctx->timer1));
+    }
+    CK(cudaEventRecord(ctx->timer0, ctx->s));
+    return TL_OK;
+}
+
+TL_API tl_status tl_timer_stop(tl_ctx* ctx, double* ms) {
+    if (!ctx || !ms || !ctx->timer0) return TL_ERR_INVALID_ARGUMENT;
+    CK(cudaEventRecord(ctx->timer1, ctx->s));
+    CK(cudaEventSynchronize(ctx->timer1));
+    float f = 0;
+    CK(cudaEventElapsedTime(&f, ctx->timer0, ctx->timer1));
+    *ms = f;
     return TL_OK;
 }
 

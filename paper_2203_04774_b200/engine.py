@@ -127,6 +127,14 @@ class Context:
         _check(self._p, _native.trigpu().tl_cost_report(self._p, out.ctypes.data))
         return out
 
+    def timer_start(self) -> None:
+        _check(self._p, _native.trigpu().tl_timer_start(self._p))
+
+    def timer_stop(self) -> float:
+        ms = C.c_double(0.0)
+        _check(self._p, _native.trigpu().tl_timer_stop(self._p, C.byref(ms)))
+        return ms.value
+
     def phase_times(self) -> dict:
         lib = _native.trigpu()
         buf = (C.c_double * 32)()
