@@ -53,57 +53,113 @@ struct ListParams {
     uint64_t bitmap_words;
 };
 
-template <int ALGO, unsigned F>
-struct Sink {
-    unsigned long long cnt = 0, sum = 0;
-    unsigned long long seed_hits = 0;
+// Per-warp hit buffer: hits (x, y) are compacted into shared memory by a
+// ballot and emitted 32 at a time with every lane busy, instead of running
+// the dense-id gathers / hash / atomics with the 1-3 lanes that hit in a batch.
+constexpr int kHitBuf = 160;  // 31 pending + up to 4 batches of 32 before a drain
+constexpr int kMetaBytes = 768;  // per warp: uint4[32] block table, u32[32] edge lanes, u32[32] x
 
-    // Called convergently by the whole warp once per 32-wide batch.
-    __device__ __forceinline__ void batch(const ListParams& P, bool hit, uint32_t seed, uint32_t x,
-                                          uint32_t y) {
-        cnt += hit;
-        if constexpr (F == 0u) return;
-        if constexpr ((F & F_VCOUNT) != 0u) {
-            if (hit) {
-                atomicAdd(&P.vcount[x], 1ull);
-                atomicAdd(&P.vcount[y], 1ull);
-                ++seed_hits;
-            }
+// Emit n (<= 32) buffered hits, lane i taking entry i; returns this lane's
+// checksum contribution. Out of line: it runs once per 32 triangles.
+template <int ALGO, unsigned F>
+__device__ __forceinline__ unsigned long long emit_hits(const ListParams& P, uint32_t seed, unsigned n,
+                                                     unsigned from) {
+    const unsigned lane = lane_id();
+    const bool hit = lane < n;
+    const uint2 e = hit ? lds64(from + 8u * lane) : make_uint2(0, 0);
+    const uint32_t x = e.x, y = e.y;
+    unsigned long long sum = 0;
+    if constexpr ((F & F_VCOUNT) != 0u) {
+        if (hit) {
+            atomicAdd(&P.vcount[x], 1ull);
+            atomicAdd(&P.vcount[y], 1ull);
         }
-        if constexpr ((F & (F_CHECKSUM | F_LIST)) != 0u) {
-            const uint32_t ru = ALGO == ALGO_APM ? seed : x;
-            const uint32_t rv = ALGO == ALGO_APM ? x : y;
-            const uint32_t rw = ALGO == ALGO_APM ? y : seed;
-            uint32_t du = 0, dv = 0, dw = 0;
+    }
+    if constexpr ((F & (F_CHECKSUM | F_LIST)) != 0u) {
+        const uint32_t ru = ALGO == ALGO_APM ? seed : x;
+        const uint32_t rv = ALGO == ALGO_APM ? x : y;
+        const uint32_t rw = ALGO == ALGO_APM ? y : seed;
+        uint32_t du = 0, dv = 0, dw = 0;
+        if (hit) {
+            du = __ldg(P.inv + ru);
+            dv = __ldg(P.inv + rv);
+            dw = __ldg(P.inv + rw);
+        }
+        if constexpr ((F & F_CHECKSUM) != 0u)
+            if (hit) sum = tri_hash(du, dv, dw);
+        if constexpr ((F & F_LIST) != 0u) {
+            unsigned long long base = 0;
+            if (lane == 0) base = atomicAdd(&P.acc[2], (unsigned long long)n);
+            base = __shfl_sync(FULL, base, 0);
             if (hit) {
-                du = P.inv[ru];
-                dv = P.inv[rv];
-                dw = P.inv[rw];
-            }
-            if constexpr ((F & F_CHECKSUM) != 0u)
-                if (hit) sum += tri_hash(du, dv, dw);
-            if constexpr ((F & F_LIST) != 0u) {
-                const unsigned b = __ballot_sync(FULL, hit);
-                if (b) {
-                    const unsigned leader = __ffs(b) - 1;
-                    unsigned long long base = 0;
-                    if (lane_id() == leader) base = atomicAdd(&P.acc[2], (unsigned long long)__popc(b));
-                    base = __shfl_sync(FULL, base, leader);
-                    if (hit) {
-                        const unsigned long long k = base + __popc(b & lanemask_lt());
-                        if (k < P.tri_cap) {
-                            P.tri[3 * k] = du;
-                            P.tri[3 * k + 1] = dv;
-                            P.tri[3 * k + 2] = dw;
-                        }
-                    }
+                const unsigned long long k = base + lane;
+                if (k < P.tri_cap) {
+                    P.tri[3 * k] = du;
+                    P.tri[3 * k + 1] = dv;
+                    P.tri[3 * k + 2] = dw;
                 }
             }
         }
     }
+    return sum;
+}
 
-    // End of one seed's unit: credit the seed's own per-vertex count.
+template <int ALGO, unsigned F>
+struct Sink {
+    unsigned long long cnt = 0, sum = 0;
+    unsigned seed_hits = 0;
+    unsigned buf = 0;      // shared address of this warp's kHitBuf uint2 entries
+    unsigned meta = 0;     // shared address of this warp's kMetaBytes row table
+    unsigned pending = 0;  // warp-uniform
+
+    // One 32-wide batch (called convergently by the whole warp).
+    __device__ __forceinline__ void batch(bool hit, uint32_t x, uint32_t y) {
+        if constexpr (F != 0u) {
+            const unsigned b = __ballot_sync(FULL, hit);
+            if (!b) return;
+            if constexpr ((F & F_VCOUNT) != 0u) seed_hits += hit;
+            if (hit) sts64(buf + 8u * (pending + __popc(b & lanemask_lt())), make_uint2(x, y));
+            pending += __popc(b);
+        }
+    }
+
+    // Same, with x read (broadcast) from shared memory only if some lane hit.
+    __device__ __forceinline__ void batch_lazy(bool hit, unsigned xaddr, uint32_t y) {
+        if constexpr (F != 0u) {
+            const unsigned b = __ballot_sync(FULL, hit);
+            if (!b) return;
+            const uint32_t x = lds32(xaddr);
+            if constexpr ((F & F_VCOUNT) != 0u) seed_hits += hit;
+            if (hit) sts64(buf + 8u * (pending + __popc(b & lanemask_lt())), make_uint2(x, y));
+            pending += __popc(b);
+        }
+    }
+
+    // Emit every full group of 32 buffered hits (call after <= 4 batches).
+    __device__ __forceinline__ void drain(const ListParams& P, uint32_t seed) {
+        if constexpr (F != 0u) {
+            if (pending < 32) return;
+            __syncwarp();
+            unsigned done = 0;
+            for (; pending - done >= 32; done += 32) sum += emit_hits<ALGO, F>(P, seed, 32, buf + 8u * done);
+            __syncwarp();
+            if (lane_id() < pending - done) sts64(buf + 8u * lane_id(), lds64(buf + 8u * (done + lane_id())));
+            __syncwarp();
+            pending -= done;
+        }
+    }
+
+    // End of one seed's unit: drain the buffer, credit the seed's own count.
     __device__ __forceinline__ void end_unit(const ListParams& P, uint32_t seed) {
+        if constexpr (F != 0u) {
+            drain(P, seed);
+            if (pending) {
+                __syncwarp();
+                sum += emit_hits<ALGO, F>(P, seed, pending, buf);
+                __syncwarp();
+                pending = 0;
+            }
+        }
         if constexpr ((F & F_VCOUNT) != 0u) {
             const unsigned long long h = warp_sum64(seed_hits);
             if (lane_id() == 0 && h) atomicAdd(&P.vcount[seed], h);
@@ -121,8 +177,20 @@ struct Sink {
     }
 };
 
-// Walk the out-rows of up to 32 x's (x valid on lanes with xvalid) as one
-// flattened stream, probing every element y against the seed's set.
+// Walk the out-rows of up to 32 x's (x valid on lanes with xvalid), probing
+// every element y against the seed's set. Two phases:
+//   1. rows of >= 32 elements, as 128-byte-ALIGNED blocks of 32 elements
+//      (partial first / last block predicated), flattened over all blocks of
+//      all such rows: block g belongs to row j = #rows whose blocks end at or
+//      before g (one vote); the row's block offset and edge lanes come from a
+//      per-warp shared-memory table read with a broadcast LDS; lane l reads
+//      element l of the block (one fully coalesced 128 B line). Software-
+//      pipelined: the next four blocks' loads are issued before the current
+//      four are probed (up to eight loads in flight per lane);
+//   2. rows of < 32 elements as ONE flattened stream (lane f of a window
+//      reads element f of the concatenated rows; the owning row of each lane
+//      comes from an OR-reduction of the row starts), so short rows do not
+//      idle lanes.
 template <int ALGO, unsigned F, class Probe>
 __device__ __forceinline__ void scan_rows(const ListParams& P, uint32_t seed, uint32_t x, bool xvalid,
                                           const Probe& probe, Sink<ALGO, F>& sink) {
@@ -133,8 +201,61 @@ __device__ __forceinline__ void scan_rows(const ListParams& P, uint32_t seed, ui
         ro = P.out_off[x];
         rl = static_cast<uint32_t>(P.out_off[x + 1] - ro);
     }
+    unsigned hits = 0;
+    // ---- phase 1: long rows as aligned blocks
+    const bool longrow = rl >= 32u;
+    if (__any_sync(FULL, longrow)) {
+        uint32_t nbl = 0;
+        uint64_t fb = 0;
+        if (longrow) {
+            fb = ro >> 5;
+            nbl = static_cast<uint32_t>(((ro + rl - 1) >> 5) - fb + 1);
+        }
+        const uint32_t bincl = warp_incl_scan(nbl);
+        const uint32_t nblocks = __shfl_sync(FULL, bincl, 31);
+        const uint32_t bstart = bincl - nbl;
+        {
+            const uint64_t boff = fb - bstart;  // absolute block = g + boff
+            sts128(sink.meta + 16u * lane,
+                   make_uint4(static_cast<uint32_t>(boff), static_cast<uint32_t>(boff >> 32), bstart,
+                              bincl - 1));
+            sts32(sink.meta + 512u + 4u * lane,
+                  (static_cast<uint32_t>(ro) & 31u) | ((static_cast<uint32_t>(ro + rl - 1) & 31u) << 8));
+            sts32(sink.meta + 640u + 4u * lane, x);
+        }
+        __syncwarp();
+        // block gi -> (row j, loaded y; kNone when masked off or past the end)
+        auto row_of = [&](uint32_t gi) { return min(__popc(__ballot_sync(FULL, bincl <= gi)), 31); };
+        auto fetch = [&](uint32_t gi) -> uint32_t {
+            const int j = row_of(gi);
+            const uint4 m = lds128(sink.meta + 16u * j);
+            const uint32_t lh = lds32(sink.meta + 512u + 4u * j);
+            const uint64_t blk = ((static_cast<uint64_t>(m.y) << 32) | m.x) + gi;
+            const bool v = gi < nblocks && (gi != m.z || lane >= (lh & 31u)) && (gi != m.w || lane <= (lh >> 8));
+            return v ? __ldg(P.out_adj + blk * 32ull + lane) : kNone;
+        };
+        constexpr int U = F ? 4 : 8;  // 128 B loads in flight per lane
+        for (uint32_t g = 0; g < nblocks; g += U) {
+            uint32_t y[U];
+#pragma unroll
+            for (int i = 0; i < U; ++i) y[i] = fetch(g + i);
+#pragma unroll
+            for (int i = 0; i < U; ++i) {
+                const bool h = probe(y[i], y[i] != kNone);
+                hits += h;
+                if constexpr (F != 0u) sink.batch_lazy(h, sink.meta + 640u + 4u * row_of(g + i), y[i]);
+            }
+            if constexpr (F != 0u) sink.drain(P, seed);
+        }
+        __syncwarp();
+        if (longrow) rl = 0;
+    }
+    // ---- phase 2: tails
     const unsigned ne = __ballot_sync(FULL, rl != 0);
-    if (!ne) return;
+    if (!ne) {
+        sink.cnt += hits;
+        return;
+    }
     // compact non-empty rows to the low lanes
     const int cnt = __popc(ne);
     const int src = lane < (unsigned)cnt ? (int)__fns(ne, 0, lane + 1) : 0;
@@ -148,24 +269,36 @@ __device__ __forceinline__ void scan_rows(const ListParams& P, uint32_t seed, ui
     const uint64_t rbase = cro - start;  // element f of the stream lives at out_adj[rbase(row) + f]
     const unsigned le = lanemask_le();
     int before = 0;
-    for (uint32_t base = 0; base < total; base += 32) {
-        const unsigned bit = (crl != 0 && start >= base && start - base < 32u) ? (1u << (start - base)) : 0u;
-        const unsigned M = __reduce_or_sync(FULL, bit);
-        int j = before + __popc(M & le) - 1;
-        before += __popc(M);
-        j = j > 31 ? 31 : j;
-        const uint32_t f = base + lane;
-        const bool act = f < total;
-        const uint64_t rb = shfl64(rbase, j);
-        const uint32_t y = act ? __ldg(P.out_adj + rb + f) : kNone;
-        const bool hit = probe(y, act);
-        if constexpr (F == 0u) {
-            sink.cnt += hit;
-        } else {
-            const uint32_t xx = __shfl_sync(FULL, cx, j);
-            sink.batch(P, hit, seed, xx, y);
+    // two 32-wide windows per iteration: both loads are in flight before the
+    // first probe
+    for (uint32_t base = 0; base < total; base += 64) {
+        const uint32_t rel = start - base;  // wraps when start < base: no bit
+        const unsigned bitA = (crl != 0 && start >= base && rel < 32u) ? (1u << rel) : 0u;
+        const unsigned bitB = (crl != 0 && start >= base && rel - 32u < 32u) ? (1u << (rel - 32u)) : 0u;
+        const unsigned MA = __reduce_or_sync(FULL, bitA);
+        const unsigned MB = __reduce_or_sync(FULL, bitB);
+        const int ca = __popc(MA);
+        int jA = before + __popc(MA & le) - 1;
+        int jB = before + ca + __popc(MB & le) - 1;
+        before += ca + __popc(MB);
+        jA = jA > 31 ? 31 : jA;
+        jB = jB > 31 ? 31 : jB;
+        const uint32_t fA = base + lane, fB = fA + 32;
+        const bool actA = fA < total, actB = fB < total;
+        const uint64_t rbA = shfl64(rbase, jA);
+        const uint64_t rbB = shfl64(rbase, jB);
+        const uint32_t yA = actA ? __ldg(P.out_adj + rbA + fA) : kNone;
+        const uint32_t yB = actB ? __ldg(P.out_adj + rbB + fB) : kNone;
+        const bool hitA = probe(yA, actA);
+        const bool hitB = probe(yB, actB);
+        hits += (unsigned)hitA + (unsigned)hitB;
+        if constexpr (F != 0u) {
+            sink.batch(hitA, __shfl_sync(FULL, cx, jA), yA);
+            sink.batch(hitB, __shfl_sync(FULL, cx, jB), yB);
+            sink.drain(P, seed);
         }
     }
+    sink.cnt += hits;
 }
 
 // ---- probes --------------------------------------------------------------
@@ -184,20 +317,88 @@ struct RegProbe {  // S sorted ascending, one element per lane, padded with kNon
     }
 };
 
-struct HashProbe {  // open addressing, linear probing, kNone = empty
-    const uint32_t* tab;
-    uint32_t mask, shift;
+// Bucketised hash table in shared memory: nb (power of two) buckets of four
+// u32 slots, one 16-byte LDS.128 per probe and no probe loop. Slots of a
+// bucket fill in order, so slot 3 occupied <=> bucket full; keys that find
+// their bucket full go to a small stash, scanned only for full buckets.
+// If even the stash overflows (never observed; needs > kStash collisions of
+// 5+ keys per bucket) the seed falls back to a binary search of its sorted
+// row in global memory, so the result stays exact.
+constexpr uint32_t kStash = 32;
+
+struct BucketTable {
+    uint32_t* slots;      // 4 * nb u32, shared memory
+    uint32_t* stash;      // kStash u32, shared memory
+    unsigned* nstash;     // shared counter (also holds the overflow flag)
+};
+
+__device__ __forceinline__ uint32_t bucket_shift(uint32_t d, uint32_t max_bits) {
+    // nb = smallest power of two >= 2d (<= 1/2 key per slot-quad on average), >= 16
+    uint32_t bits = 32 - __clz(max(2u * d - 1u, 15u));
+    bits = bits > max_bits ? max_bits : bits;
+    return 32 - bits;
+}
+
+__device__ __forceinline__ void bucket_insert(const BucketTable& T, uint32_t shift, uint32_t key) {
+    uint32_t* b = T.slots + 4u * ((key * 0x9E3779B1u) >> shift);
+#pragma unroll
+    for (int s = 0; s < 4; ++s)
+        if (atomicCAS(&b[s], kNone, key) == kNone) return;
+    const unsigned i = atomicAdd(T.nstash, 1u);
+    if (i < kStash) T.stash[i] = key;
+}
+
+__device__ __forceinline__ void bucket_clear(const BucketTable& T, uint32_t shift, uint32_t key) {
+    uint4* b = reinterpret_cast<uint4*>(T.slots) + ((key * 0x9E3779B1u) >> shift);
+    *b = make_uint4(kNone, kNone, kNone, kNone);
+}
+
+
+// Exact fallback: binary search of the seed's sorted set row (global).
+struct SearchProbe {
+    const uint32_t* row;
+    uint32_t d;
     __device__ __forceinline__ bool operator()(uint32_t y, bool act) const {
         if (!act) return false;
-        uint32_t h = slot_hash(y, shift);
-        for (;;) {
-            const uint32_t t = tab[h];
-            if (t == y) return true;
-            if (t == kNone) return false;
-            h = (h + 1) & mask;
+        uint32_t lo = 0, hi = d;
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (__ldg(row + mid) < y) lo = mid + 1;
+            else hi = mid;
         }
+        return lo < d && __ldg(row + lo) == y;
     }
 };
+
+template <bool kStashed>
+struct BucketProbe {
+    unsigned slots;   // shared address of the bucket array
+    unsigned stash;   // shared address of the stash
+    uint32_t shift;
+    uint32_t nstash;  // kStashed == false <=> nstash == 0 (the common case)
+    __device__ __forceinline__ bool operator()(uint32_t y, bool act) const {
+        const uint4 v = lds128(slots + 16u * ((y * 0x9E3779B1u) >> shift));
+        bool hit = (v.x == y) | (v.y == y) | (v.z == y) | (v.w == y);
+        if constexpr (kStashed) {
+            if (act && !hit && v.w != kNone)
+                for (uint32_t i = 0; i < nstash; ++i) hit |= lds32(stash + 4u * i) == y;
+        }
+        return act && hit;
+    }
+};
+
+// Run `body(probe)` with the probe variant the seed's table needs.
+template <class Body>
+__device__ __forceinline__ void with_bucket_probe(const BucketTable& T, uint32_t shift, unsigned ns,
+                                                  const uint32_t* row, uint32_t d, Body&& body) {
+    if (ns == 0) {
+        body(BucketProbe<false>{smem_addr(T.slots), smem_addr(T.stash), shift, 0});
+    } else if (ns <= kStash) {
+        body(BucketProbe<true>{smem_addr(T.slots), smem_addr(T.stash), shift, ns});
+    } else {
+        body(SearchProbe{row, d});
+    }
+}
 
 struct BitmapProbe {
     const uint32_t* bm;
@@ -207,22 +408,30 @@ struct BitmapProbe {
     }
 };
 
-__device__ __forceinline__ uint32_t table_bits(uint32_t d, uint32_t max_bits) {
-    // smallest power of two >= 4d (load factor <= 1/4), at least 64 slots
-    uint32_t bits = 32 - __clz(max(4u * d - 1u, 63u));
-    return bits > max_bits ? max_bits : bits;
+// ---- per-warp scratch in dynamic shared memory ------------------------------
+// [warps x kMetaBytes row tables][warps x kHitBuf uint2 hit buffers, F != 0]
+// followed by the kernel's probe tables.
+template <unsigned F>
+__host__ __device__ constexpr size_t warp_scratch_bytes(int warps) {
+    return static_cast<size_t>(warps) * (kMetaBytes + (F ? kHitBuf * 8 : 0));
 }
 
-__device__ __forceinline__ void hash_insert(uint32_t* tab, uint32_t mask, uint32_t shift, uint32_t key) {
-    uint32_t h = slot_hash(key, shift);
-    while (atomicCAS(&tab[h], kNone, key) != kNone) h = (h + 1) & mask;
+template <int ALGO, unsigned F>
+__device__ __forceinline__ void attach_scratch(Sink<ALGO, F>& sink, unsigned char* base, int warps) {
+    const unsigned w = threadIdx.x >> 5;
+    sink.meta = smem_addr(base + w * kMetaBytes);
+    if constexpr (F != 0u) sink.buf = smem_addr(base + warps * kMetaBytes + w * kHitBuf * 8);
 }
 
 // ---- class R: |S| <= 32, warp per seed, S in registers -------------------
+constexpr int kRWarps = 8;
+
 template <int ALGO, unsigned F>
-__global__ void __launch_bounds__(256) k_list_reg(ListParams P) {
+__global__ void __launch_bounds__(kRWarps * 32) k_list_reg(ListParams P) {
+    extern __shared__ __align__(16) unsigned char dsm[];
     const unsigned lane = lane_id();
     Sink<ALGO, F> sink;
+    attach_scratch(sink, dsm, kRWarps);
     for (;;) {
         unsigned i = 0;
         if (lane == 0) i = atomicAdd(P.queue, 1u);
@@ -239,18 +448,23 @@ __global__ void __launch_bounds__(256) k_list_reg(ListParams P) {
     sink.flush(P);
 }
 
-// ---- class H: 32 < |S| <= 256, warp per seed, per-warp smem hash --------
+// ---- class H: 32 < |S| <= 256, warp per seed, per-warp bucket table ----
 constexpr int kHWarps = 8;
-constexpr uint32_t kHMaxBits = 10;  // 1024 slots per warp
+constexpr uint32_t kHMaxBits = 8;  // 256 buckets = 4 KB per warp
+constexpr size_t kHTableBytes = (16u << kHMaxBits) + kStash * 4 + 16;
 
 template <int ALGO, unsigned F>
 __global__ void __launch_bounds__(kHWarps * 32) k_list_hash_warp(ListParams P) {
-    __shared__ uint32_t tabs[kHWarps][1u << kHMaxBits];
+    extern __shared__ __align__(16) unsigned char dsm[];
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
-    uint32_t* tab = tabs[warp];
-    for (uint32_t i = lane; i < (1u << kHMaxBits); i += 32) tab[i] = kNone;
+    unsigned char* tbase = dsm + warp_scratch_bytes<F>(kHWarps) + warp * kHTableBytes;
+    BucketTable T{reinterpret_cast<uint32_t*>(tbase), reinterpret_cast<uint32_t*>(tbase + (16u << kHMaxBits)),
+                  reinterpret_cast<unsigned*>(tbase + (16u << kHMaxBits) + kStash * 4)};
+    for (uint32_t i = lane; i < (4u << kHMaxBits); i += 32) T.slots[i] = kNone;
+    if (lane == 0) *T.nstash = 0;
     __syncwarp();
     Sink<ALGO, F> sink;
+    attach_scratch(sink, dsm, kHWarps);
     for (;;) {
         unsigned i = 0;
         if (lane == 0) i = atomicAdd(P.queue, 1u);
@@ -259,39 +473,48 @@ __global__ void __launch_bounds__(kHWarps * 32) k_list_hash_warp(ListParams P) {
         const uint32_t seed = P.seeds[i];
         const uint64_t so = P.set_off[seed];
         const uint32_t d = static_cast<uint32_t>(P.set_off[seed + 1] - so);
-        const uint32_t bits = table_bits(d, kHMaxBits);
-        const uint32_t mask = (1u << bits) - 1, shift = 32 - bits;
-        for (uint32_t k = lane; k < d; k += 32) hash_insert(tab, mask, shift, __ldg(P.set_adj + so + k));
+        const uint32_t shift = bucket_shift(d, kHMaxBits);
+        for (uint32_t k = lane; k < d; k += 32) bucket_insert(T, shift, __ldg(P.set_adj + so + k));
         __syncwarp();
-        HashProbe probe{tab, mask, shift};
-        for (uint32_t c = 0; c < d; c += 32) {
-            const bool xv = c + lane < d;
-            const uint32_t x = xv ? __ldg(P.set_adj + so + c + lane) : kNone;
-            scan_rows<ALGO, F>(P, seed, x, xv, probe, sink);
-        }
+        with_bucket_probe(T, shift, *T.nstash, P.set_adj + so, d, [&](const auto& probe) {
+            for (uint32_t c = 0; c < d; c += 32) {
+                const bool xv = c + lane < d;
+                const uint32_t x = xv ? __ldg(P.set_adj + so + c + lane) : kNone;
+                scan_rows<ALGO, F>(P, seed, x, xv, probe, sink);
+            }
+        });
         sink.end_unit(P, seed);
         __syncwarp();
-        for (uint32_t k = lane; k <= mask; k += 32) tab[k] = kNone;
+        for (uint32_t k = lane; k < d; k += 32) bucket_clear(T, shift, __ldg(P.set_adj + so + k));
+        if (lane == 0) *T.nstash = 0;
         __syncwarp();
     }
     sink.flush(P);
 }
 
-// ---- class C: 256 < |S| <= 4096, CTA per (seed, x-slice), smem hash ------
+// ---- class C: 256 < |S| <= 4096, CTA per (seed, x-slice), bucket table ----
 constexpr int kCThreads = 512;
-constexpr uint32_t kCMaxBits = 14;  // 16384 slots = 64 KB
+constexpr int kCWarps = kCThreads / 32;
+constexpr uint32_t kCMaxBits = 12;  // 4096 buckets = 64 KB
 constexpr uint32_t kCSlice = 1024;  // x's per unit
 constexpr uint32_t kCMaxSlices = 4096 / kCSlice;
+constexpr size_t kCTableBytes = (16u << kCMaxBits) + kStash * 4 + 16;
 
 template <int ALGO, unsigned F>
 __global__ void __launch_bounds__(kCThreads) k_list_hash_cta(ListParams P) {
-    extern __shared__ __align__(16) uint32_t ctab[];
+    extern __shared__ __align__(16) unsigned char dsm[];
     __shared__ unsigned unit;
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
-    constexpr unsigned W = kCThreads / 32;
-    for (uint32_t i = threadIdx.x; i < (1u << kCMaxBits); i += kCThreads) ctab[i] = kNone;
+    unsigned char* tbase = dsm + warp_scratch_bytes<F>(kCWarps);
+    BucketTable T{reinterpret_cast<uint32_t*>(tbase), reinterpret_cast<uint32_t*>(tbase + (16u << kCMaxBits)),
+                  reinterpret_cast<unsigned*>(tbase + (16u << kCMaxBits) + kStash * 4)};
+    for (uint32_t i = threadIdx.x; i < (4u << kCMaxBits); i += kCThreads) T.slots[i] = kNone;
+    if (threadIdx.x == 0) *T.nstash = 0;
     Sink<ALGO, F> sink;
-    uint32_t cur_seed = kNone, cur_mask = 0, cur_shift = 0;
+    attach_scratch(sink, dsm, kCWarps);
+    uint32_t cur_seed = kNone, cur_shift = 0;
+    uint64_t cur_so = 0;
+    uint32_t cur_d = 0;
     for (;;) {
         __syncthreads();
         if (threadIdx.x == 0) unit = atomicAdd(P.queue, 1u);
@@ -304,39 +527,45 @@ __global__ void __launch_bounds__(kCThreads) k_list_hash_cta(ListParams P) {
         const uint32_t d = static_cast<uint32_t>(P.set_off[seed + 1] - so);
         if (slice * kCSlice >= d) continue;  // uniform across the CTA
         if (seed != cur_seed) {
-            if (cur_seed != kNone)
-                for (uint32_t k = threadIdx.x; k <= cur_mask; k += kCThreads) ctab[k] = kNone;
+            if (cur_seed != kNone) {
+                for (uint32_t k = threadIdx.x; k < cur_d; k += kCThreads)
+                    bucket_clear(T, cur_shift, __ldg(P.set_adj + cur_so + k));
+                if (threadIdx.x == 0) *T.nstash = 0;
+            }
             __syncthreads();
-            const uint32_t bits = table_bits(d, kCMaxBits);
-            cur_mask = (1u << bits) - 1;
-            cur_shift = 32 - bits;
+            cur_shift = bucket_shift(d, kCMaxBits);
             for (uint32_t k = threadIdx.x; k < d; k += kCThreads)
-                hash_insert(ctab, cur_mask, cur_shift, __ldg(P.set_adj + so + k));
+                bucket_insert(T, cur_shift, __ldg(P.set_adj + so + k));
             cur_seed = seed;
+            cur_so = so;
+            cur_d = d;
             __syncthreads();
         }
-        HashProbe probe{ctab, cur_mask, cur_shift};
         const uint32_t xb = slice * kCSlice, xe = min(d, xb + kCSlice);
-        for (uint32_t c = xb + warp * 32; c < xe; c += W * 32) {
-            const bool xv = c + lane < xe;
-            const uint32_t x = xv ? __ldg(P.set_adj + so + c + lane) : kNone;
-            scan_rows<ALGO, F>(P, seed, x, xv, probe, sink);
-        }
+        with_bucket_probe(T, cur_shift, *T.nstash, P.set_adj + so, d, [&](const auto& probe) {
+            for (uint32_t c = xb + warp * 32; c < xe; c += kCWarps * 32) {
+                const bool xv = c + lane < xe;
+                const uint32_t x = xv ? __ldg(P.set_adj + so + c + lane) : kNone;
+                scan_rows<ALGO, F>(P, seed, x, xv, probe, sink);
+            }
+        });
         sink.end_unit(P, seed);
     }
     sink.flush(P);
 }
 
 // ---- class G: |S| > 4096, CTA per seed, global bitmap --------------------
-constexpr int kGThreads = 1024;
+constexpr int kGThreads = 512;
+constexpr int kGWarps = kGThreads / 32;
 
 template <int ALGO, unsigned F>
 __global__ void __launch_bounds__(kGThreads) k_list_giant(ListParams P) {
+    extern __shared__ __align__(16) unsigned char dsm[];
     __shared__ unsigned unit;
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
-    constexpr unsigned W = kGThreads / 32;
     uint32_t* bm = P.bitmaps + (uint64_t)blockIdx.x * P.bitmap_words;
     Sink<ALGO, F> sink;
+    attach_scratch(sink, dsm, kGWarps);
     for (;;) {
         __syncthreads();
         if (threadIdx.x == 0) unit = atomicAdd(P.queue, 1u);
@@ -352,7 +581,7 @@ __global__ void __launch_bounds__(kGThreads) k_list_giant(ListParams P) {
         }
         __syncthreads();
         BitmapProbe probe{bm};
-        for (uint32_t c = warp * 32; c < d; c += W * 32) {
+        for (uint32_t c = warp * 32; c < d; c += kGWarps * 32) {
             const bool xv = c + lane < d;
             const uint32_t x = xv ? __ldg(P.set_adj + so + c + lane) : kNone;
             scan_rows<ALGO, F>(P, seed, x, xv, probe, sink);
@@ -366,6 +595,12 @@ __global__ void __launch_bounds__(kGThreads) k_list_giant(ListParams P) {
     }
     sink.flush(P);
 }
+
+// dynamic shared memory per CTA of each class kernel
+template <unsigned F> constexpr size_t smem_reg() { return warp_scratch_bytes<F>(kRWarps); }
+template <unsigned F> constexpr size_t smem_hash_warp() { return warp_scratch_bytes<F>(kHWarps) + kHWarps * kHTableBytes; }
+template <unsigned F> constexpr size_t smem_hash_cta() { return warp_scratch_bytes<F>(kCWarps) + kCTableBytes; }
+template <unsigned F> constexpr size_t smem_giant() { return warp_scratch_bytes<F>(kGWarps); }
 
 // ---- seed classification --------------------------------------------------
 struct SeedLists {

@@ -307,17 +307,35 @@ tl_status ensure_in_csr(tl_ctx* ctx) {
     return TL_OK;
 }
 
+template <class K>
+tl_status set_smem(tl_ctx* ctx, K kernel, size_t bytes) {
+    CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    return TL_OK;
+}
+
+template <class K>
+unsigned resident_grid(tl_ctx* ctx, K kernel, int threads, size_t smem) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem) != cudaSuccess || per_sm < 1) {
+        (void)cudaGetLastError();
+        per_sm = 1;
+    }
+    return static_cast<unsigned>(per_sm * ctx->sms);
+}
+
 template <int ALGO, unsigned F>
 tl_status launch_classes(tl_ctx* ctx, ListParams base, uint32_t* const lists[4], const unsigned h[4],
                          unsigned int* queues) {
-    const int sms = ctx->sms;
+    tl_status st;
     // class G first, on the side stream: a few long CTAs overlap the rest
     if (h[3]) {
         ListParams p = base;
         p.seeds = lists[3];
         p.nseeds = h[3];
         p.queue = queues + 3;
-        const unsigned grid = std::min<unsigned>(h[3], (unsigned)sms);
+        const size_t smem = smem_giant<F>();
+        if ((st = set_smem(ctx, k_list_giant<ALGO, F>, smem)) != TL_OK) return st;
+        const unsigned grid = std::min<unsigned>(h[3], (unsigned)ctx->sms);
         p.bitmap_words = ((uint64_t)ctx->n + 31) / 32 + 32;
         const size_t bm_bytes = (size_t)grid * p.bitmap_words * 4;
         if (ctx->bitmaps.cap < bm_bytes) {
@@ -328,7 +346,7 @@ tl_status launch_classes(tl_ctx* ctx, ListParams base, uint32_t* const lists[4],
         p.bitmaps = P<uint32_t>(ctx->bitmaps);
         CK(cudaEventRecord(ctx->fork, ctx->s));
         CK(cudaStreamWaitEvent(ctx->s2, ctx->fork, 0));
-        k_list_giant<ALGO, F><<<grid, kGThreads, 0, ctx->s2>>>(p);
+        k_list_giant<ALGO, F><<<grid, kGThreads, smem, ctx->s2>>>(p);
         LAUNCHED();
         CK(cudaEventRecord(ctx->join, ctx->s2));
     }
@@ -337,7 +355,11 @@ tl_status launch_classes(tl_ctx* ctx, ListParams base, uint32_t* const lists[4],
         p.seeds = lists[0];
         p.nseeds = h[0];
         p.queue = queues + 0;
-        k_list_reg<ALGO, F><<<grid_for((uint64_t)h[0] * 32, 256, sms * 8), 256, 0, ctx->s>>>(p);
+        const size_t smem = smem_reg<F>();
+        if ((st = set_smem(ctx, k_list_reg<ALGO, F>, smem)) != TL_OK) return st;
+        const unsigned grid = std::min<unsigned>(grid_for((uint64_t)h[0] * 32, kRWarps * 32, ~0u),
+                                                 resident_grid(ctx, k_list_reg<ALGO, F>, kRWarps * 32, smem));
+        k_list_reg<ALGO, F><<<grid, kRWarps * 32, smem, ctx->s>>>(p);
         LAUNCHED();
     }
     if (h[1]) {
@@ -345,7 +367,11 @@ tl_status launch_classes(tl_ctx* ctx, ListParams base, uint32_t* const lists[4],
         p.seeds = lists[1];
         p.nseeds = h[1];
         p.queue = queues + 1;
-        k_list_hash_warp<ALGO, F><<<grid_for((uint64_t)h[1] * 32, kHWarps * 32, sms * 6), kHWarps * 32, 0, ctx->s>>>(p);
+        const size_t smem = smem_hash_warp<F>();
+        if ((st = set_smem(ctx, k_list_hash_warp<ALGO, F>, smem)) != TL_OK) return st;
+        const unsigned grid = std::min<unsigned>(grid_for((uint64_t)h[1] * 32, kHWarps * 32, ~0u),
+                                                 resident_grid(ctx, k_list_hash_warp<ALGO, F>, kHWarps * 32, smem));
+        k_list_hash_warp<ALGO, F><<<grid, kHWarps * 32, smem, ctx->s>>>(p);
         LAUNCHED();
     }
     if (h[2]) {
@@ -353,9 +379,11 @@ tl_status launch_classes(tl_ctx* ctx, ListParams base, uint32_t* const lists[4],
         p.seeds = lists[2];
         p.nseeds = h[2];
         p.queue = queues + 2;
-        const size_t smem = (1u << kCMaxBits) * 4;
-        CK(cudaFuncSetAttribute(k_list_hash_cta<ALGO, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_list_hash_cta<ALGO, F><<<std::min<unsigned>(h[2] * kCMaxSlices, sms * 3), kCThreads, smem, ctx->s>>>(p);
+        const size_t smem = smem_hash_cta<F>();
+        if ((st = set_smem(ctx, k_list_hash_cta<ALGO, F>, smem)) != TL_OK) return st;
+        const unsigned grid = std::min<unsigned>(h[2] * kCMaxSlices,
+                                                 resident_grid(ctx, k_list_hash_cta<ALGO, F>, kCThreads, smem));
+        k_list_hash_cta<ALGO, F><<<grid, kCThreads, smem, ctx->s>>>(p);
         LAUNCHED();
     }
     if (h[3]) CK(cudaStreamWaitEvent(ctx->s, ctx->join, 0));
