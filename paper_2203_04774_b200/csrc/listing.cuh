@@ -51,6 +51,7 @@ struct ListParams {
     unsigned int* queue;      // dynamic work counter
     uint32_t* bitmaps;        // class G only: one n-bit bitmap per CTA
     uint64_t bitmap_words;
+    int variant;              // probe flavour of classes H / C (0 bucket, 1 filtered bucket)
 };
 
 // Per-warp hit buffer: hits (x, y) are compacted into shared memory by a
@@ -202,53 +203,34 @@ __device__ __forceinline__ void scan_rows(const ListParams& P, uint32_t seed, ui
         rl = static_cast<uint32_t>(P.out_off[x + 1] - ro);
     }
     unsigned hits = 0;
-    // ---- phase 1: long rows as aligned blocks
-    const bool longrow = rl >= 32u;
-    if (__any_sync(FULL, longrow)) {
-        uint32_t nbl = 0;
-        uint64_t fb = 0;
-        if (longrow) {
-            fb = ro >> 5;
-            nbl = static_cast<uint32_t>(((ro + rl - 1) >> 5) - fb + 1);
-        }
+    // ---- phase 1: full 32-element blocks, flattened over the blocks of all rows
+    if (__any_sync(FULL, rl >= 32u)) {
+        const uint32_t nbl = rl >> 5;
         const uint32_t bincl = warp_incl_scan(nbl);
         const uint32_t nblocks = __shfl_sync(FULL, bincl, 31);
-        const uint32_t bstart = bincl - nbl;
-        {
-            const uint64_t boff = fb - bstart;  // absolute block = g + boff
-            sts128(sink.meta + 16u * lane,
-                   make_uint4(static_cast<uint32_t>(boff), static_cast<uint32_t>(boff >> 32), bstart,
-                              bincl - 1));
-            sts32(sink.meta + 512u + 4u * lane,
-                  (static_cast<uint32_t>(ro) & 31u) | ((static_cast<uint32_t>(ro + rl - 1) & 31u) << 8));
-            sts32(sink.meta + 640u + 4u * lane, x);
-        }
-        __syncwarp();
-        // block gi -> (row j, loaded y; kNone when masked off or past the end)
-        auto row_of = [&](uint32_t gi) { return min(__popc(__ballot_sync(FULL, bincl <= gi)), 31); };
-        auto fetch = [&](uint32_t gi) -> uint32_t {
-            const int j = row_of(gi);
-            const uint4 m = lds128(sink.meta + 16u * j);
-            const uint32_t lh = lds32(sink.meta + 512u + 4u * j);
-            const uint64_t blk = ((static_cast<uint64_t>(m.y) << 32) | m.x) + gi;
-            const bool v = gi < nblocks && (gi != m.z || lane >= (lh & 31u)) && (gi != m.w || lane <= (lh >> 8));
-            return v ? __ldg(P.out_adj + blk * 32ull + lane) : kNone;
-        };
-        constexpr int U = F ? 4 : 8;  // 128 B loads in flight per lane
+        // element l of global block g of row j sits at out_adj[bbase_j + 32 g + l]
+        const uint64_t bbase = ro - 32ull * (bincl - nbl);
+        constexpr int U = 4;
         for (uint32_t g = 0; g < nblocks; g += U) {
-            uint32_t y[U];
-#pragma unroll
-            for (int i = 0; i < U; ++i) y[i] = fetch(g + i);
+            uint32_t y[U], xs[U];
 #pragma unroll
             for (int i = 0; i < U; ++i) {
-                const bool h = probe(y[i], y[i] != kNone);
+                const uint32_t gi = g + i;
+                const int j = min(__popc(__ballot_sync(FULL, bincl <= gi)), 31);
+                const uint64_t bb = shfl64(bbase, j);
+                if constexpr (F != 0u) xs[i] = __shfl_sync(FULL, x, j);
+                y[i] = gi < nblocks ? __ldg(P.out_adj + bb + 32ull * gi + lane) : kNone;
+            }
+#pragma unroll
+            for (int i = 0; i < U; ++i) {
+                const bool h = probe(y[i], g + i < nblocks);
                 hits += h;
-                if constexpr (F != 0u) sink.batch_lazy(h, sink.meta + 640u + 4u * row_of(g + i), y[i]);
+                if constexpr (F != 0u) sink.batch(h, xs[i], y[i]);
             }
             if constexpr (F != 0u) sink.drain(P, seed);
         }
-        __syncwarp();
-        if (longrow) rl = 0;
+        ro += rl & ~31u;
+        rl &= 31u;
     }
     // ---- phase 2: tails
     const unsigned ne = __ballot_sync(FULL, rl != 0);
@@ -301,6 +283,18 @@ __device__ __forceinline__ void scan_rows(const ListParams& P, uint32_t seed, ui
     sink.cnt += hits;
 }
 
+// Chunks of 32 x's: set elements c, c + stride, ... below xe of the seed row at so.
+template <int ALGO, unsigned F, class Probe>
+__device__ __forceinline__ void scan_x_range(const ListParams& P, uint32_t seed, uint64_t so, uint32_t cb,
+                                             uint32_t xe, uint32_t stride, Probe probe, Sink<ALGO, F>& sink) {
+    const unsigned lane = lane_id();
+    for (uint32_t c = cb; c < xe; c += stride) {
+        const bool xv = c + lane < xe;
+        const uint32_t x = xv ? __ldg(P.set_adj + so + c + lane) : kNone;
+        scan_rows<ALGO, F>(P, seed, x, xv, probe, sink);
+    }
+}
+
 // ---- probes --------------------------------------------------------------
 
 struct RegProbe {  // S sorted ascending, one element per lane, padded with kNone
@@ -330,7 +324,13 @@ struct BucketTable {
     uint32_t* slots;      // 4 * nb u32, shared memory
     uint32_t* stash;      // kStash u32, shared memory
     unsigned* nstash;     // shared counter (also holds the overflow flag)
+    uint32_t* bm;         // prefilter bitmap: 32 * nb bits (nb words), shared memory
 };
+
+// Prefilter bit of a key (independent of the bucket hash); bshift = shift - 5.
+__device__ __forceinline__ uint32_t filter_bit(uint32_t key, uint32_t bshift) {
+    return (key * 0x85EBCA77u) >> bshift;
+}
 
 __device__ __forceinline__ uint32_t bucket_shift(uint32_t d, uint32_t max_bits) {
     // nb = smallest power of two >= 2d (<= 1/2 key per slot-quad on average), >= 16
@@ -340,6 +340,8 @@ __device__ __forceinline__ uint32_t bucket_shift(uint32_t d, uint32_t max_bits) 
 }
 
 __device__ __forceinline__ void bucket_insert(const BucketTable& T, uint32_t shift, uint32_t key) {
+    const uint32_t fb = filter_bit(key, shift - 5);
+    atomicOr(T.bm + (fb >> 5), 1u << (fb & 31));
     uint32_t* b = T.slots + 4u * ((key * 0x9E3779B1u) >> shift);
 #pragma unroll
     for (int s = 0; s < 4; ++s)
@@ -349,10 +351,37 @@ __device__ __forceinline__ void bucket_insert(const BucketTable& T, uint32_t shi
 }
 
 __device__ __forceinline__ void bucket_clear(const BucketTable& T, uint32_t shift, uint32_t key) {
+    T.bm[filter_bit(key, shift - 5) >> 5] = 0u;
     uint4* b = reinterpret_cast<uint4*>(T.slots) + ((key * 0x9E3779B1u) >> shift);
     *b = make_uint4(kNone, kNone, kNone, kNone);
 }
 
+
+// Same table behind a one-word bitmap prefilter: one conflict-light LDS.32
+// per lane; only lanes whose filter bit is set (hits + ~3% false positives)
+// issue the 16-byte bucket load.
+template <bool kStashed>
+struct FilteredProbe {
+    unsigned bm;      // shared address of the filter words
+    unsigned slots;
+    unsigned stash;
+    uint32_t shift;
+    uint32_t nstash;
+    __device__ __forceinline__ bool operator()(uint32_t y, bool act) const {
+        const uint32_t fb = filter_bit(y, shift - 5);
+        const uint32_t w = lds32(bm + 4u * (fb >> 5));
+        bool hit = false;
+        if (act && ((w >> (fb & 31)) & 1u)) {
+            const uint4 v = lds128(slots + 16u * ((y * 0x9E3779B1u) >> shift));
+            hit = (v.x == y) | (v.y == y) | (v.z == y) | (v.w == y);
+            if constexpr (kStashed) {
+                if (!hit && v.w != kNone)
+                    for (uint32_t i = 0; i < nstash; ++i) hit |= lds32(stash + 4u * i) == y;
+            }
+        }
+        return hit;
+    }
+};
 
 // Exact fallback: binary search of the seed's sorted set row (global).
 struct SearchProbe {
@@ -387,19 +416,6 @@ struct BucketProbe {
     }
 };
 
-// Run `body(probe)` with the probe variant the seed's table needs.
-template <class Body>
-__device__ __forceinline__ void with_bucket_probe(const BucketTable& T, uint32_t shift, unsigned ns,
-                                                  const uint32_t* row, uint32_t d, Body&& body) {
-    if (ns == 0) {
-        body(BucketProbe<false>{smem_addr(T.slots), smem_addr(T.stash), shift, 0});
-    } else if (ns <= kStash) {
-        body(BucketProbe<true>{smem_addr(T.slots), smem_addr(T.stash), shift, ns});
-    } else {
-        body(SearchProbe{row, d});
-    }
-}
-
 struct BitmapProbe {
     const uint32_t* bm;
     __device__ __forceinline__ bool operator()(uint32_t y, bool act) const {
@@ -413,14 +429,13 @@ struct BitmapProbe {
 // followed by the kernel's probe tables.
 template <unsigned F>
 __host__ __device__ constexpr size_t warp_scratch_bytes(int warps) {
-    return static_cast<size_t>(warps) * (kMetaBytes + (F ? kHitBuf * 8 : 0));
+    return static_cast<size_t>(warps) * (F ? kHitBuf * 8 : 0);
 }
 
 template <int ALGO, unsigned F>
 __device__ __forceinline__ void attach_scratch(Sink<ALGO, F>& sink, unsigned char* base, int warps) {
     const unsigned w = threadIdx.x >> 5;
-    sink.meta = smem_addr(base + w * kMetaBytes);
-    if constexpr (F != 0u) sink.buf = smem_addr(base + warps * kMetaBytes + w * kHitBuf * 8);
+    if constexpr (F != 0u) sink.buf = smem_addr(base + w * kHitBuf * 8);
 }
 
 // ---- class R: |S| <= 32, warp per seed, S in registers -------------------
@@ -451,16 +466,18 @@ __global__ void __launch_bounds__(kRWarps * 32) k_list_reg(ListParams P) {
 // ---- class H: 32 < |S| <= 256, warp per seed, per-warp bucket table ----
 constexpr int kHWarps = 8;
 constexpr uint32_t kHMaxBits = 8;  // 256 buckets = 4 KB per warp
-constexpr size_t kHTableBytes = (16u << kHMaxBits) + kStash * 4 + 16;
+constexpr size_t kHTableBytes = (16u << kHMaxBits) + (4u << kHMaxBits) + kStash * 4 + 16;
 
 template <int ALGO, unsigned F>
 __global__ void __launch_bounds__(kHWarps * 32) k_list_hash_warp(ListParams P) {
     extern __shared__ __align__(16) unsigned char dsm[];
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
     unsigned char* tbase = dsm + warp_scratch_bytes<F>(kHWarps) + warp * kHTableBytes;
-    BucketTable T{reinterpret_cast<uint32_t*>(tbase), reinterpret_cast<uint32_t*>(tbase + (16u << kHMaxBits)),
-                  reinterpret_cast<unsigned*>(tbase + (16u << kHMaxBits) + kStash * 4)};
+    BucketTable T{reinterpret_cast<uint32_t*>(tbase), reinterpret_cast<uint32_t*>(tbase + (20u << kHMaxBits)),
+                  reinterpret_cast<unsigned*>(tbase + (20u << kHMaxBits) + kStash * 4),
+                  reinterpret_cast<uint32_t*>(tbase + (16u << kHMaxBits))};
     for (uint32_t i = lane; i < (4u << kHMaxBits); i += 32) T.slots[i] = kNone;
+    for (uint32_t i = lane; i < (1u << kHMaxBits); i += 32) T.bm[i] = 0u;
     if (lane == 0) *T.nstash = 0;
     __syncwarp();
     Sink<ALGO, F> sink;
@@ -476,13 +493,17 @@ __global__ void __launch_bounds__(kHWarps * 32) k_list_hash_warp(ListParams P) {
         const uint32_t shift = bucket_shift(d, kHMaxBits);
         for (uint32_t k = lane; k < d; k += 32) bucket_insert(T, shift, __ldg(P.set_adj + so + k));
         __syncwarp();
-        with_bucket_probe(T, shift, *T.nstash, P.set_adj + so, d, [&](const auto& probe) {
-            for (uint32_t c = 0; c < d; c += 32) {
-                const bool xv = c + lane < d;
-                const uint32_t x = xv ? __ldg(P.set_adj + so + c + lane) : kNone;
-                scan_rows<ALGO, F>(P, seed, x, xv, probe, sink);
-            }
-        });
+        const unsigned ns = *T.nstash;
+        if (ns == 0 && P.variant == 1)
+            scan_x_range<ALGO, F>(P, seed, so, 0, d, 32,
+                                  FilteredProbe<false>{smem_addr(T.bm), smem_addr(T.slots), 0, shift, 0}, sink);
+        else if (ns == 0)
+            scan_x_range<ALGO, F>(P, seed, so, 0, d, 32, BucketProbe<false>{smem_addr(T.slots), 0, shift, 0}, sink);
+        else if (ns <= kStash)
+            scan_x_range<ALGO, F>(P, seed, so, 0, d, 32,
+                                  BucketProbe<true>{smem_addr(T.slots), smem_addr(T.stash), shift, ns}, sink);
+        else
+            scan_x_range<ALGO, F>(P, seed, so, 0, d, 32, SearchProbe{P.set_adj + so, d}, sink);
         sink.end_unit(P, seed);
         __syncwarp();
         for (uint32_t k = lane; k < d; k += 32) bucket_clear(T, shift, __ldg(P.set_adj + so + k));
@@ -498,7 +519,7 @@ constexpr int kCWarps = kCThreads / 32;
 constexpr uint32_t kCMaxBits = 12;  // 4096 buckets = 64 KB
 constexpr uint32_t kCSlice = 1024;  // x's per unit
 constexpr uint32_t kCMaxSlices = 4096 / kCSlice;
-constexpr size_t kCTableBytes = (16u << kCMaxBits) + kStash * 4 + 16;
+constexpr size_t kCTableBytes = (16u << kCMaxBits) + (4u << kCMaxBits) + kStash * 4 + 16;
 
 template <int ALGO, unsigned F>
 __global__ void __launch_bounds__(kCThreads) k_list_hash_cta(ListParams P) {
@@ -506,9 +527,11 @@ __global__ void __launch_bounds__(kCThreads) k_list_hash_cta(ListParams P) {
     __shared__ unsigned unit;
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
     unsigned char* tbase = dsm + warp_scratch_bytes<F>(kCWarps);
-    BucketTable T{reinterpret_cast<uint32_t*>(tbase), reinterpret_cast<uint32_t*>(tbase + (16u << kCMaxBits)),
-                  reinterpret_cast<unsigned*>(tbase + (16u << kCMaxBits) + kStash * 4)};
+    BucketTable T{reinterpret_cast<uint32_t*>(tbase), reinterpret_cast<uint32_t*>(tbase + (20u << kCMaxBits)),
+                  reinterpret_cast<unsigned*>(tbase + (20u << kCMaxBits) + kStash * 4),
+                  reinterpret_cast<uint32_t*>(tbase + (16u << kCMaxBits))};
     for (uint32_t i = threadIdx.x; i < (4u << kCMaxBits); i += kCThreads) T.slots[i] = kNone;
+    for (uint32_t i = threadIdx.x; i < (1u << kCMaxBits); i += kCThreads) T.bm[i] = 0u;
     if (threadIdx.x == 0) *T.nstash = 0;
     Sink<ALGO, F> sink;
     attach_scratch(sink, dsm, kCWarps);
@@ -542,13 +565,19 @@ __global__ void __launch_bounds__(kCThreads) k_list_hash_cta(ListParams P) {
             __syncthreads();
         }
         const uint32_t xb = slice * kCSlice, xe = min(d, xb + kCSlice);
-        with_bucket_probe(T, cur_shift, *T.nstash, P.set_adj + so, d, [&](const auto& probe) {
-            for (uint32_t c = xb + warp * 32; c < xe; c += kCWarps * 32) {
-                const bool xv = c + lane < xe;
-                const uint32_t x = xv ? __ldg(P.set_adj + so + c + lane) : kNone;
-                scan_rows<ALGO, F>(P, seed, x, xv, probe, sink);
-            }
-        });
+        const unsigned ns = *T.nstash;
+        const uint32_t cb = xb + warp * 32;
+        if (ns == 0 && P.variant == 1)
+            scan_x_range<ALGO, F>(P, seed, so, cb, xe, kCWarps * 32,
+                                  FilteredProbe<false>{smem_addr(T.bm), smem_addr(T.slots), 0, cur_shift, 0}, sink);
+        else if (ns == 0)
+            scan_x_range<ALGO, F>(P, seed, so, cb, xe, kCWarps * 32,
+                                  BucketProbe<false>{smem_addr(T.slots), 0, cur_shift, 0}, sink);
+        else if (ns <= kStash)
+            scan_x_range<ALGO, F>(P, seed, so, cb, xe, kCWarps * 32,
+                                  BucketProbe<true>{smem_addr(T.slots), smem_addr(T.stash), cur_shift, ns}, sink);
+        else
+            scan_x_range<ALGO, F>(P, seed, so, cb, xe, kCWarps * 32, SearchProbe{P.set_adj + so, d}, sink);
         sink.end_unit(P, seed);
     }
     sink.flush(P);
@@ -581,11 +610,7 @@ __global__ void __launch_bounds__(kGThreads) k_list_giant(ListParams P) {
         }
         __syncthreads();
         BitmapProbe probe{bm};
-        for (uint32_t c = warp * 32; c < d; c += kGWarps * 32) {
-            const bool xv = c + lane < d;
-            const uint32_t x = xv ? __ldg(P.set_adj + so + c + lane) : kNone;
-            scan_rows<ALGO, F>(P, seed, x, xv, probe, sink);
-        }
+        scan_x_range<ALGO, F>(P, seed, so, warp * 32, d, kGWarps * 32, probe, sink);
         sink.end_unit(P, seed);
         __syncthreads();
         for (uint32_t k = threadIdx.x; k < d; k += kGThreads) {

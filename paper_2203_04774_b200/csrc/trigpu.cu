@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -76,6 +77,7 @@ struct tl_ctx {
     DevBuf goff, gadj, rank, inv, radj, out_off, out_adj, in_off, in_adj, outdeg, indeg, lists, acc,
         vcount, tri, scan_part, bitmaps, small;
     bool have_vcounts = false, have_tri = false;
+    int variant = 0;  // probe flavour (TRIGPU_VARIANT), for A/B measurement
     unsigned long long tri_count = 0;
 
     tl_status fail(tl_status st, const std::string& what) {
@@ -202,7 +204,7 @@ tl_status orient_core(tl_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* goff,
     ENSURE(outdeg, (size_t)n * 4);
     ENSURE(indeg, (size_t)n * 4);
     ENSURE(out_off, ((size_t)n + 1) * 8);
-    ENSURE(out_adj, m * 4);
+    ENSURE(out_adj, m * 4 + 64);  // +16 words: bulk copies round row ends up to 16 B
     ENSURE(lists, (size_t)n * 16);
     ENSURE(small, 64);
     auto* flags = static_cast<unsigned long long*>(ctx->small.p);  // [0] err, [4..] scratch
@@ -435,6 +437,7 @@ TL_API tl_status tl_create(tl_ctx** out, int device) {
     tl_ctx* ctx = new tl_ctx();
     ctx->device = device;
     ctx->sms = prop.multiProcessorCount;
+    if (const char* v = std::getenv("TRIGPU_VARIANT")) ctx->variant = std::atoi(v);
     if ((e = cudaSetDevice(device)) != cudaSuccess || (e = cudaStreamCreateWithFlags(&ctx->s, cudaStreamNonBlocking)) != cudaSuccess ||
         (e = cudaStreamCreateWithFlags(&ctx->s2, cudaStreamNonBlocking)) != cudaSuccess) {
         g_create_error = std::string("tl_create: ") + cudaGetErrorString(e);
@@ -551,6 +554,7 @@ TL_API tl_status tl_list(tl_ctx* ctx, int algo, unsigned out_flags, tl_stats* ou
     base.inv = P<uint32_t>(ctx->inv);
     base.acc = acc;
     base.vcount = want_vc ? P<unsigned long long>(ctx->vcount) : nullptr;
+    base.variant = ctx->variant;
 
     CK(cudaEventRecord(ctx->ev[PH_COUNT + 3], ctx->s));
     CK(cudaMemsetAsync(counts, 0, 8 * sizeof(unsigned int), ctx->s));
