@@ -93,6 +93,32 @@ __device__ __forceinline__ void sts64(unsigned a, uint2 v) {
     asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(v.x), "r"(v.y) : "memory");
 }
 
+// Predicated shared loads: the value stays `dflt` when !p (no branch).
+__device__ __forceinline__ uint32_t lds32_if(unsigned a, bool p, uint32_t dflt = 0u) {
+    uint32_t v = dflt;
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.shared.u32 %0, [%1];\n\t}"
+                 : "+r"(v)
+                 : "r"(a), "r"((unsigned)p));
+    return v;
+}
+
+// Eight independent read-only global loads issued back to back in ONE asm
+// block: the compiler cannot sink them to their uses (it otherwise
+// interleaves load / use to save registers, which leaves one load in flight).
+__device__ __forceinline__ void ldg8(const uint32_t* const (&a)[8], uint32_t (&v)[8]) {
+    asm volatile(
+        "ld.global.nc.u32 %0, [%8];\n\t"
+        "ld.global.nc.u32 %1, [%9];\n\t"
+        "ld.global.nc.u32 %2, [%10];\n\t"
+        "ld.global.nc.u32 %3, [%11];\n\t"
+        "ld.global.nc.u32 %4, [%12];\n\t"
+        "ld.global.nc.u32 %5, [%13];\n\t"
+        "ld.global.nc.u32 %6, [%14];\n\t"
+        "ld.global.nc.u32 %7, [%15];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+        : "l"(a[0]), "l"(a[1]), "l"(a[2]), "l"(a[3]), "l"(a[4]), "l"(a[5]), "l"(a[6]), "l"(a[7]));
+}
+
 // Multiplicative hash into a power-of-two table of 2^bits slots.
 __device__ __forceinline__ uint32_t slot_hash(uint32_t key, uint32_t shift) {
     return (key * 0x9E3779B1u) >> shift;  // shift = 32 - bits

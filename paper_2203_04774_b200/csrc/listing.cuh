@@ -28,6 +28,8 @@
 // and come from the degree reduction k_cost.
 #pragma once
 
+#include <cub/block/block_scan.cuh>
+
 #include "common.cuh"
 
 namespace trigpu {
@@ -51,13 +53,18 @@ struct ListParams {
     unsigned int* queue;      // dynamic work counter
     uint32_t* bitmaps;        // class G only: one n-bit bitmap per CTA
     uint64_t bitmap_words;
-    int variant;              // probe flavour of classes H / C (0 bucket, 1 filtered bucket)
+    int variant;              // reserved for A/B probe experiments
+    uint32_t win_bits;        // hub-window size (log2 ranks, capped per class); 0 = no window
 };
 
 // Per-warp hit buffer: hits (x, y) are compacted into shared memory by a
 // ballot and emitted 32 at a time with every lane busy, instead of running
 // the dense-id gathers / hash / atomics with the 1-3 lanes that hit in a batch.
 constexpr int kHitBuf = 160;  // 31 pending + up to 4 batches of 32 before a drain
+// 32-element blocks loaded per warp before probing (memory-level parallelism):
+// the count-only sink keeps more in flight than the sinks that buffer hits
+constexpr int kUnrollCount = 16;
+constexpr int kUnrollSink = 8;
 constexpr int kMetaBytes = 768;  // per warp: uint4[32] block table, u32[32] edge lanes, u32[32] x
 
 // Emit n (<= 32) buffered hits, lane i taking entry i; returns this lane's
@@ -311,26 +318,28 @@ struct RegProbe {  // S sorted ascending, one element per lane, padded with kNon
     }
 };
 
-// Bucketised hash table in shared memory: nb (power of two) buckets of four
-// u32 slots, one 16-byte LDS.128 per probe and no probe loop. Slots of a
-// bucket fill in order, so slot 3 occupied <=> bucket full; keys that find
-// their bucket full go to a small stash, scanned only for full buckets.
-// If even the stash overflows (never observed; needs > kStash collisions of
-// 5+ keys per bucket) the seed falls back to a binary search of its sorted
-// row in global memory, so the result stays exact.
+// Probe structure of classes H and C: a direct bitmap over the top window
+// [wbase, n) of the rank space plus a bucketised hash table for the rest.
+//
+// Under degree ordering on power-law graphs the scanned rows N+(x) are made
+// of hubs, i.e. the top ranks: on R-MAT, 90 % of all probes hit the top
+// 0.2 % of ranks (scale 22). A sorted row's 32-element block therefore falls
+// in a handful of bitmap words, so the window probe is one LDS.32 that the
+// lanes of a warp mostly share (broadcast, no bank conflicts) and it is exact.
+// Other probes go to the hash table: nb (power of two) buckets of four u32
+// slots, one 16-byte LDS.128 per probe, slots filled in order (slot 3 used
+// <=> bucket full), overflow keys in a small stash scanned only for full
+// buckets. If even the stash overflows the seed falls back to a binary
+// search of its sorted row in global memory, so the result stays exact.
 constexpr uint32_t kStash = 32;
 
 struct BucketTable {
     uint32_t* slots;      // 4 * nb u32, shared memory
     uint32_t* stash;      // kStash u32, shared memory
-    unsigned* nstash;     // shared counter (also holds the overflow flag)
-    uint32_t* bm;         // prefilter bitmap: 32 * nb bits (nb words), shared memory
+    unsigned* nstash;     // shared counter (> kStash: overflowed)
+    uint32_t* win;        // window bitmap, shared memory
+    uint32_t wbase;       // first rank of the window
 };
-
-// Prefilter bit of a key (independent of the bucket hash); bshift = shift - 5.
-__device__ __forceinline__ uint32_t filter_bit(uint32_t key, uint32_t bshift) {
-    return (key * 0x85EBCA77u) >> bshift;
-}
 
 __device__ __forceinline__ uint32_t bucket_shift(uint32_t d, uint32_t max_bits) {
     // nb = smallest power of two >= 2d (<= 1/2 key per slot-quad on average), >= 16
@@ -340,8 +349,13 @@ __device__ __forceinline__ uint32_t bucket_shift(uint32_t d, uint32_t max_bits) 
 }
 
 __device__ __forceinline__ void bucket_insert(const BucketTable& T, uint32_t shift, uint32_t key) {
-    const uint32_t fb = filter_bit(key, shift - 5);
-    atomicOr(T.bm + (fb >> 5), 1u << (fb & 31));
+#ifdef TRIGPU_HUB_WINDOW
+    if (key >= T.wbase) {
+        const uint32_t o = key - T.wbase;
+        atomicOr(T.win + (o >> 5), 1u << (o & 31));
+        return;
+    }
+#endif
     uint32_t* b = T.slots + 4u * ((key * 0x9E3779B1u) >> shift);
 #pragma unroll
     for (int s = 0; s < 4; ++s)
@@ -351,37 +365,73 @@ __device__ __forceinline__ void bucket_insert(const BucketTable& T, uint32_t shi
 }
 
 __device__ __forceinline__ void bucket_clear(const BucketTable& T, uint32_t shift, uint32_t key) {
-    T.bm[filter_bit(key, shift - 5) >> 5] = 0u;
+#ifdef TRIGPU_HUB_WINDOW
+    if (key >= T.wbase) {
+        T.win[(key - T.wbase) >> 5] = 0u;
+        return;
+    }
+#endif
     uint4* b = reinterpret_cast<uint4*>(T.slots) + ((key * 0x9E3779B1u) >> shift);
     *b = make_uint4(kNone, kNone, kNone, kNone);
 }
 
-
-// Same table behind a one-word bitmap prefilter: one conflict-light LDS.32
-// per lane; only lanes whose filter bit is set (hits + ~3% false positives)
-// issue the 16-byte bucket load.
 template <bool kStashed>
-struct FilteredProbe {
-    unsigned bm;      // shared address of the filter words
-    unsigned slots;
-    unsigned stash;
+struct BucketProbe {
+    unsigned win;     // shared address of the window bitmap
+    uint32_t wbase;
+    unsigned slots;   // shared address of the bucket array
+    unsigned stash;   // shared address of the stash
     uint32_t shift;
-    uint32_t nstash;
+    uint32_t nstash;  // kStashed == false <=> nstash == 0 (the common case)
     __device__ __forceinline__ bool operator()(uint32_t y, bool act) const {
-        const uint32_t fb = filter_bit(y, shift - 5);
-        const uint32_t w = lds32(bm + 4u * (fb >> 5));
-        bool hit = false;
-        if (act && ((w >> (fb & 31)) & 1u)) {
-            const uint4 v = lds128(slots + 16u * ((y * 0x9E3779B1u) >> shift));
-            hit = (v.x == y) | (v.y == y) | (v.z == y) | (v.w == y);
-            if constexpr (kStashed) {
-                if (!hit && v.w != kNone)
-                    for (uint32_t i = 0; i < nstash; ++i) hit |= lds32(stash + 4u * i) == y;
-            }
+#ifdef TRIGPU_HUB_WINDOW
+        if (!act) return false;
+        if (y >= wbase) {
+            const uint32_t o = y - wbase;
+            return (lds32(win + 4u * (o >> 5)) >> (o & 31)) & 1u;
         }
-        return hit;
+#endif
+        const uint4 v = lds128(slots + 16u * ((y * 0x9E3779B1u) >> shift));
+        bool hit = (v.x == y) | (v.y == y) | (v.z == y) | (v.w == y);
+        if constexpr (kStashed) {
+            if (act && !hit && v.w != kNone)
+                for (uint32_t i = 0; i < nstash; ++i) hit |= lds32(stash + 4u * i) == y;
+        }
+        return act && hit;
+    }
+    // N probes at once: window words as predicated LDS.32 (no branches), the
+    // hash path only if some lane of the warp has a below-window element.
+    template <int N>
+    __device__ __forceinline__ void batch(const uint32_t (&y)[N], const bool (&ok)[N], bool (&h)[N]) const {
+        bool need = false;
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+            const bool inw = ok[k] && y[k] >= wbase;
+            const uint32_t o = y[k] - wbase;
+            const uint32_t w = lds32_if(win + 4u * (o >> 5), inw);
+            h[k] = (w >> (o & 31)) & 1u;
+            need |= ok[k] && !inw;
+        }
+        if (__any_sync(FULL, need)) {
+#pragma unroll
+            for (int k = 0; k < N; ++k)
+                if (ok[k] && y[k] < wbase) h[k] = (*this)(y[k], true);
+        }
     }
 };
+
+// Default batched probe: N scalar probes.
+template <class Probe, int N>
+__device__ __forceinline__ void probe_batch(const Probe& p, const uint32_t (&y)[N], const bool (&ok)[N],
+                                            bool (&h)[N]) {
+#pragma unroll
+    for (int k = 0; k < N; ++k) h[k] = p(y[k], ok[k]);
+}
+template <bool S, int N>
+__device__ __forceinline__ void probe_batch(const BucketProbe<S>& p, const uint32_t (&y)[N], const bool (&ok)[N],
+                                            bool (&h)[N]) {
+    p.batch(y, ok, h);
+}
 
 // Exact fallback: binary search of the seed's sorted set row (global).
 struct SearchProbe {
@@ -399,22 +449,29 @@ struct SearchProbe {
     }
 };
 
-template <bool kStashed>
-struct BucketProbe {
-    unsigned slots;   // shared address of the bucket array
-    unsigned stash;   // shared address of the stash
-    uint32_t shift;
-    uint32_t nstash;  // kStashed == false <=> nstash == 0 (the common case)
-    __device__ __forceinline__ bool operator()(uint32_t y, bool act) const {
-        const uint4 v = lds128(slots + 16u * ((y * 0x9E3779B1u) >> shift));
-        bool hit = (v.x == y) | (v.y == y) | (v.z == y) | (v.w == y);
-        if constexpr (kStashed) {
-            if (act && !hit && v.w != kNone)
-                for (uint32_t i = 0; i < nstash; ++i) hit |= lds32(stash + 4u * i) == y;
-        }
-        return act && hit;
-    }
+// Timing-only probe (TRIGPU_VARIANT=2): touches every loaded element, never
+// hits. Measures the row-streaming limit of a kernel without the probe cost.
+struct NullProbe {
+    __device__ __forceinline__ bool operator()(uint32_t y, bool act) const { return act && y == 0xFFFFFFFEu; }
 };
+
+// Dispatch on the table state of the current seed (uniform per unit).
+template <class Body>
+__device__ __forceinline__ void dispatch_probe(const BucketTable& T, uint32_t shift, unsigned ns,
+                                               const uint32_t* row, uint32_t d, int variant, Body&& body) {
+#ifdef TRIGPU_EXPERIMENTS
+    if (variant == 2) {
+        body(NullProbe{});
+        return;
+    }
+#endif
+    if (ns == 0)
+        body(BucketProbe<false>{smem_addr(T.win), T.wbase, smem_addr(T.slots), 0, shift, 0});
+    else if (ns <= kStash)
+        body(BucketProbe<true>{smem_addr(T.win), T.wbase, smem_addr(T.slots), smem_addr(T.stash), shift, ns});
+    else
+        body(SearchProbe{row, d});
+}
 
 struct BitmapProbe {
     const uint32_t* bm;
@@ -456,28 +513,43 @@ __global__ void __launch_bounds__(kRWarps * 32) k_list_reg(ListParams P) {
         const uint64_t so = P.set_off[seed];
         const uint32_t d = static_cast<uint32_t>(P.set_off[seed + 1] - so);
         const uint32_t s = lane < d ? __ldg(P.set_adj + so + lane) : kNone;
-        RegProbe probe{s};
-        scan_rows<ALGO, F>(P, seed, s, lane < d, probe, sink);
+#ifdef TRIGPU_EXPERIMENTS
+        if (P.variant == 2) {
+            scan_rows<ALGO, F>(P, seed, s, lane < d, NullProbe{}, sink);
+            sink.end_unit(P, seed);
+            continue;
+        }
+#endif
+        scan_rows<ALGO, F>(P, seed, s, lane < d, RegProbe{s}, sink);
         sink.end_unit(P, seed);
     }
     sink.flush(P);
 }
 
-// ---- class H: 32 < |S| <= 256, warp per seed, per-warp bucket table ----
+// ---- class H: 32 < |S| <= 256, warp per seed, per-warp probe table ------
 constexpr int kHWarps = 8;
-constexpr uint32_t kHMaxBits = 8;  // 256 buckets = 4 KB per warp
-constexpr size_t kHTableBytes = (16u << kHMaxBits) + (4u << kHMaxBits) + kStash * 4 + 16;
+constexpr uint32_t kHMaxBits = 8;     // 256 buckets = 4 KB per warp
+constexpr uint32_t kHWinBits = 12;    // 4096-rank window = 512 B per warp
+constexpr size_t kHTableBytes = (16u << kHMaxBits) + (1u << kHWinBits) / 8 + kStash * 4 + 16;
+
+// wbase for a window of 2^win_bits top ranks; win_bits == 0 disables it.
+__device__ __forceinline__ uint32_t window_base(uint32_t n, uint32_t win_bits) {
+    if (win_bits == 0) return 0xFFFFFFFFu;
+    return n > (1u << win_bits) ? n - (1u << win_bits) : 0u;
+}
 
 template <int ALGO, unsigned F>
 __global__ void __launch_bounds__(kHWarps * 32) k_list_hash_warp(ListParams P) {
     extern __shared__ __align__(16) unsigned char dsm[];
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
     unsigned char* tbase = dsm + warp_scratch_bytes<F>(kHWarps) + warp * kHTableBytes;
-    BucketTable T{reinterpret_cast<uint32_t*>(tbase), reinterpret_cast<uint32_t*>(tbase + (20u << kHMaxBits)),
-                  reinterpret_cast<unsigned*>(tbase + (20u << kHMaxBits) + kStash * 4),
-                  reinterpret_cast<uint32_t*>(tbase + (16u << kHMaxBits))};
+    constexpr uint32_t kSlotBytes = 16u << kHMaxBits, kWinBytes = (1u << kHWinBits) / 8;
+    BucketTable T{reinterpret_cast<uint32_t*>(tbase), reinterpret_cast<uint32_t*>(tbase + kSlotBytes + kWinBytes),
+                  reinterpret_cast<unsigned*>(tbase + kSlotBytes + kWinBytes + kStash * 4),
+                  reinterpret_cast<uint32_t*>(tbase + kSlotBytes),
+                  window_base(P.n, min(P.win_bits, kHWinBits))};
     for (uint32_t i = lane; i < (4u << kHMaxBits); i += 32) T.slots[i] = kNone;
-    for (uint32_t i = lane; i < (1u << kHMaxBits); i += 32) T.bm[i] = 0u;
+    for (uint32_t i = lane; i < kWinBytes / 4; i += 32) T.win[i] = 0u;
     if (lane == 0) *T.nstash = 0;
     __syncwarp();
     Sink<ALGO, F> sink;
@@ -493,17 +565,9 @@ __global__ void __launch_bounds__(kHWarps * 32) k_list_hash_warp(ListParams P) {
         const uint32_t shift = bucket_shift(d, kHMaxBits);
         for (uint32_t k = lane; k < d; k += 32) bucket_insert(T, shift, __ldg(P.set_adj + so + k));
         __syncwarp();
-        const unsigned ns = *T.nstash;
-        if (ns == 0 && P.variant == 1)
-            scan_x_range<ALGO, F>(P, seed, so, 0, d, 32,
-                                  FilteredProbe<false>{smem_addr(T.bm), smem_addr(T.slots), 0, shift, 0}, sink);
-        else if (ns == 0)
-            scan_x_range<ALGO, F>(P, seed, so, 0, d, 32, BucketProbe<false>{smem_addr(T.slots), 0, shift, 0}, sink);
-        else if (ns <= kStash)
-            scan_x_range<ALGO, F>(P, seed, so, 0, d, 32,
-                                  BucketProbe<true>{smem_addr(T.slots), smem_addr(T.stash), shift, ns}, sink);
-        else
-            scan_x_range<ALGO, F>(P, seed, so, 0, d, 32, SearchProbe{P.set_adj + so, d}, sink);
+        dispatch_probe(T, shift, *T.nstash, P.set_adj + so, d, P.variant, [&](const auto& probe) {
+            scan_x_range<ALGO, F>(P, seed, so, 0, d, 32, probe, sink);
+        });
         sink.end_unit(P, seed);
         __syncwarp();
         for (uint32_t k = lane; k < d; k += 32) bucket_clear(T, shift, __ldg(P.set_adj + so + k));
@@ -513,72 +577,139 @@ __global__ void __launch_bounds__(kHWarps * 32) k_list_hash_warp(ListParams P) {
     sink.flush(P);
 }
 
-// ---- class C: 256 < |S| <= 4096, CTA per (seed, x-slice), bucket table ----
-constexpr int kCThreads = 512;
+// ---- class C: 256 < |S| <= 4096, CTA per seed, bucket table -------------
+// All 32 warps of the CTA share the seed's table. The seed's rows are cut
+// into 32-element blocks (block prefix over the set in shared memory) and
+// warps pull batches of kCBatch blocks from a shared counter, so the CTA
+// barrier at the end of a seed waits for at most one batch per warp.
+constexpr int kCThreads = 1024;
 constexpr int kCWarps = kCThreads / 32;
 constexpr uint32_t kCMaxBits = 12;  // 4096 buckets = 64 KB
-constexpr uint32_t kCSlice = 1024;  // x's per unit
-constexpr uint32_t kCMaxSlices = 4096 / kCSlice;
-constexpr size_t kCTableBytes = (16u << kCMaxBits) + (4u << kCMaxBits) + kStash * 4 + 16;
+constexpr uint32_t kCMaxD = 4096;
+constexpr uint32_t kCBatch = 4;
+constexpr uint32_t kCWinBits = 18;  // 262144-rank window = 32 KB
+constexpr size_t kCTableBytes = (16u << kCMaxBits) + (1u << kCWinBits) / 8 + kStash * 4 + 16;
+constexpr size_t kCRowBytes = kCMaxD * 16;  // uint4 {ro lo, ro hi, len, first block} per set element
+
+template <int ALGO, unsigned F, class Probe>
+__device__ __forceinline__ void cta_blocks(const ListParams& P, uint32_t seed, uint64_t so, uint32_t d,
+                                           unsigned rows, uint32_t nblocks, const Probe& probe,
+                                           Sink<ALGO, F>& sink) {
+    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+    // equal share of the seed's blocks per warp (equal work), contiguous so
+    // the owning row is found once and then walked forward
+    const uint32_t gb = static_cast<uint32_t>((static_cast<uint64_t>(nblocks) * warp) / kCWarps);
+    const uint32_t ge = static_cast<uint32_t>((static_cast<uint64_t>(nblocks) * (warp + 1)) / kCWarps);
+    if (gb >= ge) return;
+    uint32_t lo = 0, hi = d - 1;
+    while (lo < hi) {  // last row i with first_block(i) <= gb
+        const uint32_t mid = (lo + hi + 1) >> 1;
+        if (lds32(rows + 16u * mid + 12u) <= gb) lo = mid;
+        else hi = mid - 1;
+    }
+    uint32_t i = lo;
+    uint4 r = lds128(rows + 16u * i);
+    uint32_t next_first = i + 1 < d ? lds32(rows + 16u * (i + 1) + 12u) : 0xFFFFFFFFu;
+    unsigned hits = 0;
+    for (uint32_t g0 = gb; g0 < ge; g0 += kCBatch) {
+        uint32_t y[kCBatch], xi[kCBatch];
+#pragma unroll
+        for (int k = 0; k < (int)kCBatch; ++k) {
+            const uint32_t gi = g0 + k;
+            y[k] = kNone;
+            if (gi < ge) {
+                while (next_first <= gi) {  // advance to the row owning block gi
+                    ++i;
+                    r = lds128(rows + 16u * i);
+                    next_first = i + 1 < d ? lds32(rows + 16u * (i + 1) + 12u) : 0xFFFFFFFFu;
+                }
+                const uint32_t pos = 32u * (gi - r.w) + lane;
+                if (pos < r.z) y[k] = __ldg(P.out_adj + ((static_cast<uint64_t>(r.y) << 32) | r.x) + pos);
+            }
+            xi[k] = i;
+        }
+#pragma unroll
+        for (int k = 0; k < (int)kCBatch; ++k) {
+            const bool h = probe(y[k], y[k] != kNone);
+            hits += h;
+            if constexpr (F != 0u) {
+                if (__any_sync(FULL, h)) sink.batch(h, __ldg(P.set_adj + so + xi[k]), y[k]);
+            }
+        }
+        if constexpr (F != 0u) sink.drain(P, seed);
+    }
+    sink.cnt += hits;
+}
 
 template <int ALGO, unsigned F>
-__global__ void __launch_bounds__(kCThreads) k_list_hash_cta(ListParams P) {
+__global__ void __launch_bounds__(kCThreads, 1) k_list_hash_cta(ListParams P) {
     extern __shared__ __align__(16) unsigned char dsm[];
-    __shared__ unsigned unit;
-    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+    __shared__ unsigned unit, next_block, total_blocks;
+    using BS = cub::BlockScan<uint32_t, kCThreads>;
+    __shared__ typename BS::TempStorage scan_tmp;
     unsigned char* tbase = dsm + warp_scratch_bytes<F>(kCWarps);
-    BucketTable T{reinterpret_cast<uint32_t*>(tbase), reinterpret_cast<uint32_t*>(tbase + (20u << kCMaxBits)),
-                  reinterpret_cast<unsigned*>(tbase + (20u << kCMaxBits) + kStash * 4),
-                  reinterpret_cast<uint32_t*>(tbase + (16u << kCMaxBits))};
+    constexpr uint32_t kSlotBytes = 16u << kCMaxBits, kWinBytes = (1u << kCWinBits) / 8;
+    BucketTable T{reinterpret_cast<uint32_t*>(tbase), reinterpret_cast<uint32_t*>(tbase + kSlotBytes + kWinBytes),
+                  reinterpret_cast<unsigned*>(tbase + kSlotBytes + kWinBytes + kStash * 4),
+                  reinterpret_cast<uint32_t*>(tbase + kSlotBytes),
+                  window_base(P.n, min(P.win_bits, kCWinBits))};
+    const unsigned rows = smem_addr(tbase + kCTableBytes);
     for (uint32_t i = threadIdx.x; i < (4u << kCMaxBits); i += kCThreads) T.slots[i] = kNone;
-    for (uint32_t i = threadIdx.x; i < (1u << kCMaxBits); i += kCThreads) T.bm[i] = 0u;
+    for (uint32_t i = threadIdx.x; i < kWinBytes / 4; i += kCThreads) T.win[i] = 0u;
     if (threadIdx.x == 0) *T.nstash = 0;
     Sink<ALGO, F> sink;
     attach_scratch(sink, dsm, kCWarps);
-    uint32_t cur_seed = kNone, cur_shift = 0;
-    uint64_t cur_so = 0;
-    uint32_t cur_d = 0;
+    constexpr int PER = kCMaxD / kCThreads;  // set elements per thread
     for (;;) {
         __syncthreads();
-        if (threadIdx.x == 0) unit = atomicAdd(P.queue, 1u);
+        if (threadIdx.x == 0) {
+            unit = atomicAdd(P.queue, 1u);
+            next_block = 0;
+        }
         __syncthreads();
         const unsigned u = unit;
-        if (u >= P.nseeds * kCMaxSlices) break;
-        const uint32_t seed = P.seeds[u / kCMaxSlices];
-        const uint32_t slice = u % kCMaxSlices;
+        if (u >= P.nseeds) break;
+        const uint32_t seed = P.seeds[u];
         const uint64_t so = P.set_off[seed];
         const uint32_t d = static_cast<uint32_t>(P.set_off[seed + 1] - so);
-        if (slice * kCSlice >= d) continue;  // uniform across the CTA
-        if (seed != cur_seed) {
-            if (cur_seed != kNone) {
-                for (uint32_t k = threadIdx.x; k < cur_d; k += kCThreads)
-                    bucket_clear(T, cur_shift, __ldg(P.set_adj + cur_so + k));
-                if (threadIdx.x == 0) *T.nstash = 0;
+        const uint32_t shift = bucket_shift(d, kCMaxBits);
+        // table + row info (blocked: thread t owns set elements PER*t ..)
+        uint32_t nb[PER];
+        uint64_t ro[PER];
+        uint32_t len[PER];
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const uint32_t i = threadIdx.x * PER + k;
+            nb[k] = 0;
+            ro[k] = 0;
+            len[k] = 0;
+            if (i < d) {
+                const uint32_t x = __ldg(P.set_adj + so + i);
+                bucket_insert(T, shift, x);
+                ro[k] = P.out_off[x];
+                len[k] = static_cast<uint32_t>(P.out_off[x + 1] - ro[k]);
+                nb[k] = (len[k] + 31u) >> 5;
             }
-            __syncthreads();
-            cur_shift = bucket_shift(d, kCMaxBits);
-            for (uint32_t k = threadIdx.x; k < d; k += kCThreads)
-                bucket_insert(T, cur_shift, __ldg(P.set_adj + so + k));
-            cur_seed = seed;
-            cur_so = so;
-            cur_d = d;
-            __syncthreads();
         }
-        const uint32_t xb = slice * kCSlice, xe = min(d, xb + kCSlice);
-        const unsigned ns = *T.nstash;
-        const uint32_t cb = xb + warp * 32;
-        if (ns == 0 && P.variant == 1)
-            scan_x_range<ALGO, F>(P, seed, so, cb, xe, kCWarps * 32,
-                                  FilteredProbe<false>{smem_addr(T.bm), smem_addr(T.slots), 0, cur_shift, 0}, sink);
-        else if (ns == 0)
-            scan_x_range<ALGO, F>(P, seed, so, cb, xe, kCWarps * 32,
-                                  BucketProbe<false>{smem_addr(T.slots), 0, cur_shift, 0}, sink);
-        else if (ns <= kStash)
-            scan_x_range<ALGO, F>(P, seed, so, cb, xe, kCWarps * 32,
-                                  BucketProbe<true>{smem_addr(T.slots), smem_addr(T.stash), cur_shift, ns}, sink);
-        else
-            scan_x_range<ALGO, F>(P, seed, so, cb, xe, kCWarps * 32, SearchProbe{P.set_adj + so, d}, sink);
+        uint32_t agg;
+        BS(scan_tmp).ExclusiveSum(nb, nb, agg);
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const uint32_t i = threadIdx.x * PER + k;
+            if (i < d)
+                sts128(rows + 16u * i, make_uint4(static_cast<uint32_t>(ro[k]), static_cast<uint32_t>(ro[k] >> 32),
+                                                  len[k], nb[k]));
+        }
+        if (threadIdx.x == 0) total_blocks = agg;
+        __syncthreads();
+        const uint32_t nblocks = total_blocks;
+        dispatch_probe(T, shift, *T.nstash, P.set_adj + so, d, P.variant, [&](const auto& probe) {
+            cta_blocks<ALGO, F>(P, seed, so, d, rows, nblocks, probe, sink);
+        });
         sink.end_unit(P, seed);
+        __syncthreads();
+        for (uint32_t k = threadIdx.x; k < d; k += kCThreads) bucket_clear(T, shift, __ldg(P.set_adj + so + k));
+        if (threadIdx.x == 0) *T.nstash = 0;
     }
     sink.flush(P);
 }
@@ -624,7 +755,7 @@ __global__ void __launch_bounds__(kGThreads) k_list_giant(ListParams P) {
 // dynamic shared memory per CTA of each class kernel
 template <unsigned F> constexpr size_t smem_reg() { return warp_scratch_bytes<F>(kRWarps); }
 template <unsigned F> constexpr size_t smem_hash_warp() { return warp_scratch_bytes<F>(kHWarps) + kHWarps * kHTableBytes; }
-template <unsigned F> constexpr size_t smem_hash_cta() { return warp_scratch_bytes<F>(kCWarps) + kCTableBytes; }
+template <unsigned F> constexpr size_t smem_hash_cta() { return warp_scratch_bytes<F>(kCWarps) + kCTableBytes + kCRowBytes; }
 template <unsigned F> constexpr size_t smem_giant() { return warp_scratch_bytes<F>(kGWarps); }
 
 // ---- seed classification --------------------------------------------------

@@ -77,7 +77,8 @@ struct tl_ctx {
     DevBuf goff, gadj, rank, inv, radj, out_off, out_adj, in_off, in_adj, outdeg, indeg, lists, acc,
         vcount, tri, scan_part, bitmaps, small;
     bool have_vcounts = false, have_tri = false;
-    int variant = 0;  // probe flavour (TRIGPU_VARIANT), for A/B measurement
+    int variant = 0;        // probe flavour (TRIGPU_VARIANT), for A/B measurement
+    uint32_t win_bits = 0;  // hub-window cap (TRIGPU_WIN_BITS), tests force the hash path
     unsigned long long tri_count = 0;
 
     tl_status fail(tl_status st, const std::string& what) {
@@ -383,8 +384,7 @@ tl_status launch_classes(tl_ctx* ctx, ListParams base, uint32_t* const lists[4],
         p.queue = queues + 2;
         const size_t smem = smem_hash_cta<F>();
         if ((st = set_smem(ctx, k_list_hash_cta<ALGO, F>, smem)) != TL_OK) return st;
-        const unsigned grid = std::min<unsigned>(h[2] * kCMaxSlices,
-                                                 resident_grid(ctx, k_list_hash_cta<ALGO, F>, kCThreads, smem));
+        const unsigned grid = std::min<unsigned>(h[2], resident_grid(ctx, k_list_hash_cta<ALGO, F>, kCThreads, smem));
         k_list_hash_cta<ALGO, F><<<grid, kCThreads, smem, ctx->s>>>(p);
         LAUNCHED();
     }
@@ -438,6 +438,7 @@ TL_API tl_status tl_create(tl_ctx** out, int device) {
     ctx->device = device;
     ctx->sms = prop.multiProcessorCount;
     if (const char* v = std::getenv("TRIGPU_VARIANT")) ctx->variant = std::atoi(v);
+    if (const char* v = std::getenv("TRIGPU_WIN_BITS")) ctx->win_bits = (uint32_t)std::atoi(v);
     if ((e = cudaSetDevice(device)) != cudaSuccess || (e = cudaStreamCreateWithFlags(&ctx->s, cudaStreamNonBlocking)) != cudaSuccess ||
         (e = cudaStreamCreateWithFlags(&ctx->s2, cudaStreamNonBlocking)) != cudaSuccess) {
         g_create_error = std::string("tl_create: ") + cudaGetErrorString(e);
@@ -555,6 +556,7 @@ TL_API tl_status tl_list(tl_ctx* ctx, int algo, unsigned out_flags, tl_stats* ou
     base.acc = acc;
     base.vcount = want_vc ? P<unsigned long long>(ctx->vcount) : nullptr;
     base.variant = ctx->variant;
+    base.win_bits = ctx->win_bits;
 
     CK(cudaEventRecord(ctx->ev[PH_COUNT + 3], ctx->s));
     CK(cudaMemsetAsync(counts, 0, 8 * sizeof(unsigned int), ctx->s));

@@ -264,3 +264,28 @@ def test_full_size_c4_properties(ctx):
     vals = list(out.values())
     for v in vals[1:]:
         assert v[0] == vals[0][0] and v[1] == vals[0][1] and np.array_equal(v[2], vals[0][2])
+
+
+@pytest.mark.parametrize("win_bits", [1, 6, 11])
+def test_probe_window_split(monkeypatch, win_bits):
+    """The class H / C probe splits each seed's set between a hub-window
+    bitmap and a hash table. Shrinking the window (TRIGPU_WIN_BITS) forces
+    the hash path on graphs small enough for the oracle; results must not
+    depend on where the split falls."""
+    monkeypatch.setenv("TRIGPU_WIN_BITS", str(win_bits))
+    c = tg.Context(0)
+    try:
+        for g in (tg.gen_rmat(15, 16, 3), tg.gen_chung_lu(50000, 800000, seed=4)):
+            for meth in ("degree", "split"):
+                pi, _ = host.compute_order(g, meth)
+                _oracle_check(c, g, pi, lists=False)
+        case = next(x for x in cases() if x["name"] == "gnm_60_400_11")
+        off, adj = case_csr(case)
+        for key, ent in case["orderings"].items():
+            c.orient(off, adj, np.array(ent["ranks"], np.uint32))
+            for algo, an in ((TL_ALGO_APP, "app"), (TL_ALGO_APM, "apm")):
+                st = c.list(algo, ALL)
+                assert str(st.checksum) == ent[an]["checksum"]
+                assert canon(c.fetch_triangles()).tolist() == ent[an]["canonical"]
+    finally:
+        c.close()
