@@ -35,6 +35,12 @@ $(LIB)/libtrigpu.so: $(CU_SRCS) $(CU_HDRS)
 	@mkdir -p $(LIB)
 	$(NVCC) $(NVFLAGS) -Xptxas -v -shared $(CU_SRCS) -o $@ -lcudart_static -lrt -ldl -lpthread 2> build_ptxas.log || (cat build_ptxas.log; exit 1)
 
+# experimental build with the hub-window probe (A/B timing via TRIGPU_LIB_SUFFIX=_win)
+gpu_win: $(LIB)/libtrigpu_win.so
+$(LIB)/libtrigpu_win.so: $(CU_SRCS) $(CU_HDRS)
+	@mkdir -p $(LIB)
+	$(NVCC) $(NVFLAGS) -DTRIGPU_HUB_WINDOW -DTRIGPU_EXPERIMENTS -shared $(CU_SRCS) -o $@ -lcudart_static -lrt -ldl -lpthread
+
 $(LIB)/libtrihost.so: $(CSRC)/host/trihost.cpp $(CSRC)/host/trihost.h $(REF_HOST_SRCS)
 	@mkdir -p $(LIB)
 	$(CXX) -std=c++20 -O3 -fPIC -shared -I$(REF)/core/include -I$(CSRC)/host \

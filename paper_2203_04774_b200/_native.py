@@ -16,7 +16,8 @@ from functools import lru_cache
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_DIR = os.path.join(_HERE, "lib")
-TRIGPU_PATH = os.path.join(LIB_DIR, "libtrigpu.so")
+# TRIGPU_LIB_SUFFIX selects an experimental build (e.g. "_win") for A/B timing
+TRIGPU_PATH = os.path.join(LIB_DIR, "libtrigpu%s.so" % os.environ.get("TRIGPU_LIB_SUFFIX", ""))
 TRIHOST_PATH = os.path.join(LIB_DIR, "libtrihost.so")
 
 # include/trigpu.h

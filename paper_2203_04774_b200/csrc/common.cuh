@@ -119,6 +119,16 @@ __device__ __forceinline__ void ldg8(const uint32_t* const (&a)[8], uint32_t (&v
         : "l"(a[0]), "l"(a[1]), "l"(a[2]), "l"(a[3]), "l"(a[4]), "l"(a[5]), "l"(a[6]), "l"(a[7]));
 }
 
+__device__ __forceinline__ void ldg4(const uint32_t* const (&a)[4], uint32_t (&v)[4]) {
+    asm volatile(
+        "ld.global.nc.u32 %0, [%4];\n\t"
+        "ld.global.nc.u32 %1, [%5];\n\t"
+        "ld.global.nc.u32 %2, [%6];\n\t"
+        "ld.global.nc.u32 %3, [%7];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+        : "l"(a[0]), "l"(a[1]), "l"(a[2]), "l"(a[3]));
+}
+
 // Multiplicative hash into a power-of-two table of 2^bits slots.
 __device__ __forceinline__ uint32_t slot_hash(uint32_t key, uint32_t shift) {
     return (key * 0x9E3779B1u) >> shift;  // shift = 32 - bits

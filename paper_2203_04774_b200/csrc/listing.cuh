@@ -185,6 +185,41 @@ struct Sink {
     }
 };
 
+// Probe the elements of blocks [kb, ke) of one row (base rp, len elements;
+// block k = elements 32k .. 32k+31, lane l takes element 32k + l): four
+// blocks' loads issued back to back, then probed; the row end is predicated.
+template <int ALGO, unsigned F, class Probe>
+__device__ __forceinline__ void stream_blocks(const ListParams& P, uint32_t seed, const uint32_t* rp, uint32_t len,
+                                              uint32_t kb, uint32_t ke, uint32_t x, const Probe& probe,
+                                              Sink<ALGO, F>& sink, unsigned& hits) {
+    const unsigned lane = lane_id();
+    const uint32_t* p = rp + 32u * kb + lane;
+    uint32_t pos = 32u * kb + lane;
+    for (uint32_t k = kb; k < ke; k += 4) {
+        const uint32_t* a[4];
+        uint32_t y[4];
+        bool ok[4], h[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            ok[i] = k + i < ke && pos + 32u * i < len;
+            a[i] = ok[i] ? p + 32 * i : rp;
+        }
+        ldg4(a, y);
+        probe_batch(probe, y, ok, h);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) hits += h[i];
+        if constexpr (F != 0u) {
+            if (__any_sync(FULL, h[0] | h[1] | h[2] | h[3])) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) sink.batch(h[i], x, y[i]);
+                sink.drain(P, seed);
+            }
+        }
+        p += 128;
+        pos += 128;
+    }
+}
+
 // Walk the out-rows of up to 32 x's (x valid on lanes with xvalid), probing
 // every element y against the seed's set. Two phases:
 //   1. rows of >= 32 elements, as 128-byte-ALIGNED blocks of 32 elements
@@ -210,35 +245,16 @@ __device__ __forceinline__ void scan_rows(const ListParams& P, uint32_t seed, ui
         rl = static_cast<uint32_t>(P.out_off[x + 1] - ro);
     }
     unsigned hits = 0;
-    // ---- phase 1: full 32-element blocks, flattened over the blocks of all rows
-    if (__any_sync(FULL, rl >= 32u)) {
-        const uint32_t nbl = rl >> 5;
-        const uint32_t bincl = warp_incl_scan(nbl);
-        const uint32_t nblocks = __shfl_sync(FULL, bincl, 31);
-        // element l of global block g of row j sits at out_adj[bbase_j + 32 g + l]
-        const uint64_t bbase = ro - 32ull * (bincl - nbl);
-        constexpr int U = 4;
-        for (uint32_t g = 0; g < nblocks; g += U) {
-            uint32_t y[U], xs[U];
-#pragma unroll
-            for (int i = 0; i < U; ++i) {
-                const uint32_t gi = g + i;
-                const int j = min(__popc(__ballot_sync(FULL, bincl <= gi)), 31);
-                const uint64_t bb = shfl64(bbase, j);
-                if constexpr (F != 0u) xs[i] = __shfl_sync(FULL, x, j);
-                y[i] = gi < nblocks ? __ldg(P.out_adj + bb + 32ull * gi + lane) : kNone;
-            }
-#pragma unroll
-            for (int i = 0; i < U; ++i) {
-                const bool h = probe(y[i], g + i < nblocks);
-                hits += h;
-                if constexpr (F != 0u) sink.batch(h, xs[i], y[i]);
-            }
-            if constexpr (F != 0u) sink.drain(P, seed);
-        }
-        ro += rl & ~31u;
-        rl &= 31u;
+    // ---- phase 1: rows of >= 32 elements, one at a time, whole warp per row
+    unsigned longm = __ballot_sync(FULL, rl >= 32u);
+    while (longm) {
+        const int j = __ffs(longm) - 1;
+        longm &= longm - 1;
+        const uint32_t len = __shfl_sync(FULL, rl, j);
+        const uint32_t* rp = P.out_adj + shfl64(ro, j);
+        stream_blocks<ALGO, F>(P, seed, rp, len, 0, (len + 31u) >> 5, __shfl_sync(FULL, x, j), probe, sink, hits);
     }
+    if (rl >= 32u) rl = 0;
     // ---- phase 2: tails
     const unsigned ne = __ballot_sync(FULL, rl != 0);
     if (!ne) {
@@ -403,6 +419,11 @@ struct BucketProbe {
     // hash path only if some lane of the warp has a below-window element.
     template <int N>
     __device__ __forceinline__ void batch(const uint32_t (&y)[N], const bool (&ok)[N], bool (&h)[N]) const {
+#ifndef TRIGPU_HUB_WINDOW
+#pragma unroll
+        for (int k = 0; k < N; ++k) h[k] = (*this)(y[k], ok[k]);
+        return;
+#endif
         bool need = false;
 #pragma unroll
         for (int k = 0; k < N; ++k) {
@@ -529,7 +550,7 @@ __global__ void __launch_bounds__(kRWarps * 32) k_list_reg(ListParams P) {
 // ---- class H: 32 < |S| <= 256, warp per seed, per-warp probe table ------
 constexpr int kHWarps = 8;
 constexpr uint32_t kHMaxBits = 8;     // 256 buckets = 4 KB per warp
-constexpr uint32_t kHWinBits = 12;    // 4096-rank window = 512 B per warp
+constexpr uint32_t kHWinBits = 13;    // 8192-rank window = 1 KB per warp
 constexpr size_t kHTableBytes = (16u << kHMaxBits) + (1u << kHWinBits) / 8 + kStash * 4 + 16;
 
 // wbase for a window of 2^win_bits top ranks; win_bits == 0 disables it.
@@ -595,9 +616,9 @@ template <int ALGO, unsigned F, class Probe>
 __device__ __forceinline__ void cta_blocks(const ListParams& P, uint32_t seed, uint64_t so, uint32_t d,
                                            unsigned rows, uint32_t nblocks, const Probe& probe,
                                            Sink<ALGO, F>& sink) {
-    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+    const unsigned warp = threadIdx.x >> 5;
     // equal share of the seed's blocks per warp (equal work), contiguous so
-    // the owning row is found once and then walked forward
+    // the owning rows are found once and then walked forward
     const uint32_t gb = static_cast<uint32_t>((static_cast<uint64_t>(nblocks) * warp) / kCWarps);
     const uint32_t ge = static_cast<uint32_t>((static_cast<uint64_t>(nblocks) * (warp + 1)) / kCWarps);
     if (gb >= ge) return;
@@ -607,36 +628,16 @@ __device__ __forceinline__ void cta_blocks(const ListParams& P, uint32_t seed, u
         if (lds32(rows + 16u * mid + 12u) <= gb) lo = mid;
         else hi = mid - 1;
     }
-    uint32_t i = lo;
-    uint4 r = lds128(rows + 16u * i);
-    uint32_t next_first = i + 1 < d ? lds32(rows + 16u * (i + 1) + 12u) : 0xFFFFFFFFu;
     unsigned hits = 0;
-    for (uint32_t g0 = gb; g0 < ge; g0 += kCBatch) {
-        uint32_t y[kCBatch], xi[kCBatch];
-#pragma unroll
-        for (int k = 0; k < (int)kCBatch; ++k) {
-            const uint32_t gi = g0 + k;
-            y[k] = kNone;
-            if (gi < ge) {
-                while (next_first <= gi) {  // advance to the row owning block gi
-                    ++i;
-                    r = lds128(rows + 16u * i);
-                    next_first = i + 1 < d ? lds32(rows + 16u * (i + 1) + 12u) : 0xFFFFFFFFu;
-                }
-                const uint32_t pos = 32u * (gi - r.w) + lane;
-                if (pos < r.z) y[k] = __ldg(P.out_adj + ((static_cast<uint64_t>(r.y) << 32) | r.x) + pos);
-            }
-            xi[k] = i;
-        }
-#pragma unroll
-        for (int k = 0; k < (int)kCBatch; ++k) {
-            const bool h = probe(y[k], y[k] != kNone);
-            hits += h;
-            if constexpr (F != 0u) {
-                if (__any_sync(FULL, h)) sink.batch(h, __ldg(P.set_adj + so + xi[k]), y[k]);
-            }
-        }
-        if constexpr (F != 0u) sink.drain(P, seed);
+    for (uint32_t i = lo, g = gb; g < ge && i < d; ++i) {
+        const uint4 r = lds128(rows + 16u * i);  // {ro lo, ro hi, len, first block}
+        const uint32_t nb = (r.z + 31u) >> 5;
+        if (r.w + nb <= g) continue;  // empty row (or already covered)
+        const uint32_t kb = g - r.w, ke = min(ge - r.w, nb);
+        const uint32_t x = F ? __ldg(P.set_adj + so + i) : 0u;
+        stream_blocks<ALGO, F>(P, seed, P.out_adj + ((static_cast<uint64_t>(r.y) << 32) | r.x), r.z, kb, ke, x,
+                               probe, sink, hits);
+        g = r.w + ke;
     }
     sink.cnt += hits;
 }

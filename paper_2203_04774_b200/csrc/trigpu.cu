@@ -78,7 +78,11 @@ struct tl_ctx {
         vcount, tri, scan_part, bitmaps, small;
     bool have_vcounts = false, have_tri = false;
     int variant = 0;        // probe flavour (TRIGPU_VARIANT), for A/B measurement
-    uint32_t win_bits = 0;  // hub-window cap (TRIGPU_WIN_BITS), tests force the hash path
+#ifdef TRIGPU_HUB_WINDOW
+    uint32_t win_bits = 32;  // hub window on (capped per class); TRIGPU_WIN_BITS overrides
+#else
+    uint32_t win_bits = 0;   // no hub window in this build
+#endif
     unsigned long long tri_count = 0;
 
     tl_status fail(tl_status st, const std::string& what) {
