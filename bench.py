@@ -127,15 +127,21 @@ class ClockSampler:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
 
 
-def dist_setup():
+def dist_setup(backend: str = "nccl"):
+    """One process per GPU (torchrun env). The listing path does not shard
+    (north star: one GPU, no collectives), so ranks are independent replicas;
+    the process group only carries the barrier and the max-over-ranks time."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     return world, rank, local
 
 
@@ -144,9 +150,16 @@ def allreduce_max(x: float, world: int) -> float:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def replica_value(units_per_rank: float, elapsed_ms: float, world: int) -> float:
+    """Whole-job throughput of N replicas: all ranks' units over the
+    max-over-ranks device time."""
+    return world * units_per_rank / (allreduce_max(elapsed_ms, world) / 1e3)
 
 
 def barrier(world: int):
@@ -305,9 +318,9 @@ def trigpu_arm(args, cfg, world, rank, local):
     torch.cuda.synchronize()
     clocks = sampler.stop()
     barrier(world)
+    value = replica_value(T * args.steps, total_ms, world)
     total_ms = allreduce_max(total_ms, world)
     ms_per_step = total_ms / args.steps
-    value = world * T * args.steps / (total_ms / 1e3)
 
     # --- e2e through the C-ABI with pinned host buffers --------------------------
     ctx.host_register(g.offsets)
