@@ -76,7 +76,7 @@ typedef struct {
     double orient_ms;   /* device time of the last tl_orient (relabel+CSR+sort) */
     double list_ms;     /* device time of the listing kernels (ListingStats::wall_ms analogue) */
     double h2d_ms;      /* host->device copy time of the last tl_orient (0 for _device) */
-    uint64_t kernel_launches; /* kernels launched by the last orient + list */
+    uint64_t kernel_launches; /* kernels launched by the last tl_orient + this tl_list */
 } tl_stats;
 
 TL_API int tl_version(void);

@@ -129,6 +129,17 @@ __device__ __forceinline__ void ldg4(const uint32_t* const (&a)[4], uint32_t (&v
         : "l"(a[0]), "l"(a[1]), "l"(a[2]), "l"(a[3]));
 }
 
+// Ampere-style asynchronous 4-byte copies global -> shared (LDGSTS): the
+// data in flight lives in shared memory, not in registers.
+__device__ __forceinline__ void cp_async4(unsigned dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // Multiplicative hash into a power-of-two table of 2^bits slots.
 __device__ __forceinline__ uint32_t slot_hash(uint32_t key, uint32_t shift) {
     return (key * 0x9E3779B1u) >> shift;  // shift = 32 - bits

@@ -117,7 +117,8 @@ struct Sink {
     unsigned long long cnt = 0, sum = 0;
     unsigned seed_hits = 0;
     unsigned buf = 0;      // shared address of this warp's kHitBuf uint2 entries
-    unsigned meta = 0;     // shared address of this warp's kMetaBytes row table
+    unsigned meta = 0;     // (unused)
+    unsigned ring = 0;     // shared address of this warp's cp.async ring (kRing x 128 B)
     unsigned pending = 0;  // warp-uniform
 
     // One 32-wide batch (called convergently by the whole warp).
@@ -188,35 +189,48 @@ struct Sink {
 // Probe the elements of blocks [kb, ke) of one row (base rp, len elements;
 // block k = elements 32k .. 32k+31, lane l takes element 32k + l): four
 // blocks' loads issued back to back, then probed; the row end is predicated.
+#ifndef TRIGPU_STREAM_U
+#define TRIGPU_STREAM_U 4
+#endif
+__device__ __forceinline__ void ldg_batch(const uint32_t* const (&a)[4], uint32_t (&y)[4]) { ldg4(a, y); }
+__device__ __forceinline__ void ldg_batch(const uint32_t* const (&a)[8], uint32_t (&y)[8]) { ldg8(a, y); }
+
 template <int ALGO, unsigned F, class Probe>
 __device__ __forceinline__ void stream_blocks(const ListParams& P, uint32_t seed, const uint32_t* rp, uint32_t len,
                                               uint32_t kb, uint32_t ke, uint32_t x, const Probe& probe,
                                               Sink<ALGO, F>& sink, unsigned& hits) {
+    constexpr int U = TRIGPU_STREAM_U;
     const unsigned lane = lane_id();
     const uint32_t* p = rp + 32u * kb + lane;
     uint32_t pos = 32u * kb + lane;
-    for (uint32_t k = kb; k < ke; k += 4) {
-        const uint32_t* a[4];
-        uint32_t y[4];
-        bool ok[4], h[4];
+    for (uint32_t k = kb; k < ke; k += U) {
+        const uint32_t* a[U];
+        uint32_t y[U];
+        bool ok[U], h[U];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < U; ++i) {
             ok[i] = k + i < ke && pos + 32u * i < len;
             a[i] = ok[i] ? p + 32 * i : rp;
         }
-        ldg4(a, y);
+        ldg_batch(a, y);
         probe_batch(probe, y, ok, h);
+        bool any = false;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) hits += h[i];
+        for (int i = 0; i < U; ++i) {
+            hits += h[i];
+            any |= h[i];
+        }
         if constexpr (F != 0u) {
-            if (__any_sync(FULL, h[0] | h[1] | h[2] | h[3])) {
+            if (__any_sync(FULL, any)) {
 #pragma unroll
-                for (int i = 0; i < 4; ++i) sink.batch(h[i], x, y[i]);
-                sink.drain(P, seed);
+                for (int i = 0; i < U; ++i) {
+                    sink.batch(h[i], x, y[i]);
+                    if (i % 4 == 3) sink.drain(P, seed);
+                }
             }
         }
-        p += 128;
-        pos += 128;
+        p += 32 * U;
+        pos += 32 * U;
     }
 }
 
@@ -505,15 +519,22 @@ struct BitmapProbe {
 // ---- per-warp scratch in dynamic shared memory ------------------------------
 // [warps x kMetaBytes row tables][warps x kHitBuf uint2 hit buffers, F != 0]
 // followed by the kernel's probe tables.
+#ifndef TRIGPU_RING
+#define TRIGPU_RING 0
+#endif
+constexpr uint32_t kRing = 8;  // blocks in flight per warp (power of two)
+constexpr size_t kRingBytes = TRIGPU_RING ? kRing * 128 : 0;
+
 template <unsigned F>
 __host__ __device__ constexpr size_t warp_scratch_bytes(int warps) {
-    return static_cast<size_t>(warps) * (F ? kHitBuf * 8 : 0);
+    return static_cast<size_t>(warps) * ((F ? kHitBuf * 8 : 0) + kRingBytes);
 }
 
 template <int ALGO, unsigned F>
 __device__ __forceinline__ void attach_scratch(Sink<ALGO, F>& sink, unsigned char* base, int warps) {
     const unsigned w = threadIdx.x >> 5;
     if constexpr (F != 0u) sink.buf = smem_addr(base + w * kHitBuf * 8);
+    sink.ring = smem_addr(base + warps * (F ? kHitBuf * 8 : 0) + w * kRingBytes);
 }
 
 // ---- class R: |S| <= 32, warp per seed, S in registers -------------------
@@ -603,24 +624,40 @@ __global__ void __launch_bounds__(kHWarps * 32) k_list_hash_warp(ListParams P) {
 // into 32-element blocks (block prefix over the set in shared memory) and
 // warps pull batches of kCBatch blocks from a shared counter, so the CTA
 // barrier at the end of a seed waits for at most one batch per warp.
-constexpr int kCThreads = 1024;
-constexpr int kCWarps = kCThreads / 32;
-constexpr uint32_t kCMaxBits = 12;  // 4096 buckets = 64 KB
-constexpr uint32_t kCMaxD = 4096;
+// Two sizes: C1 (256 < |S| <= 1024) runs 8-warp CTAs, several per SM, so one
+// CTA's seed barrier is hidden by the others; C2 (1024 < |S| <= 4096) needs
+// the 64 KB table and runs one 32-warp CTA per SM.
+template <int THREADS, uint32_t MAXBITS, uint32_t MAXD, int MINB>
+struct CtaCfg {
+    static constexpr int kThreads = THREADS;
+    static constexpr int kWarps = THREADS / 32;
+    static constexpr uint32_t kMaxBits = MAXBITS;  // 2^MAXBITS buckets
+    static constexpr uint32_t kMaxD = MAXD;
+    static constexpr int kMinBlocks = MINB;
+};
+using CfgC1 = CtaCfg<256, 11, 1024, 3>;
+using CfgC2 = CtaCfg<1024, 12, 4096, 1>;
 constexpr uint32_t kCBatch = 4;
 constexpr uint32_t kCWinBits = 18;  // 262144-rank window = 32 KB
-constexpr size_t kCTableBytes = (16u << kCMaxBits) + (1u << kCWinBits) / 8 + kStash * 4 + 16;
-constexpr size_t kCRowBytes = kCMaxD * 16;  // uint4 {ro lo, ro hi, len, first block} per set element
+#ifdef TRIGPU_HUB_WINDOW
+constexpr uint32_t kCWinBytes = (1u << kCWinBits) / 8;
+#else
+constexpr uint32_t kCWinBytes = 16;
+#endif
+template <class CFG>
+constexpr size_t cta_table_bytes() { return (16u << CFG::kMaxBits) + kCWinBytes + kStash * 4 + 16; }
+template <class CFG>
+constexpr size_t cta_row_bytes() { return CFG::kMaxD * 16; }  // uint4 {ro lo, ro hi, len, first block}
 
-template <int ALGO, unsigned F, class Probe>
+template <int ALGO, unsigned F, class CFG, class Probe>
 __device__ __forceinline__ void cta_blocks(const ListParams& P, uint32_t seed, uint64_t so, uint32_t d,
                                            unsigned rows, uint32_t nblocks, const Probe& probe,
                                            Sink<ALGO, F>& sink) {
     const unsigned warp = threadIdx.x >> 5;
     // equal share of the seed's blocks per warp (equal work), contiguous so
     // the owning rows are found once and then walked forward
-    const uint32_t gb = static_cast<uint32_t>((static_cast<uint64_t>(nblocks) * warp) / kCWarps);
-    const uint32_t ge = static_cast<uint32_t>((static_cast<uint64_t>(nblocks) * (warp + 1)) / kCWarps);
+    const uint32_t gb = static_cast<uint32_t>((static_cast<uint64_t>(nblocks) * warp) / CFG::kWarps);
+    const uint32_t ge = static_cast<uint32_t>((static_cast<uint64_t>(nblocks) * (warp + 1)) / CFG::kWarps);
     if (gb >= ge) return;
     uint32_t lo = 0, hi = d - 1;
     while (lo < hi) {  // last row i with first_block(i) <= gb
@@ -629,6 +666,54 @@ __device__ __forceinline__ void cta_blocks(const ListParams& P, uint32_t seed, u
         else hi = mid - 1;
     }
     unsigned hits = 0;
+#if TRIGPU_RING
+    // kRing blocks in flight per warp through cp.async into a shared-memory
+    // ring (lane l copies and later reads only its own word of each slot),
+    // so the depth costs no registers. Two cursors walk the rows: one issues
+    // block g + kRing while the other consumes block g.
+    const unsigned ring = sink.ring;
+    const unsigned lane = lane_id();
+    uint32_t ii = lo, ci = lo;
+    uint4 ir = lds128(rows + 16u * lo), cr = ir;
+    uint32_t inext = lo + 1 < d ? lds32(rows + 16u * (lo + 1) + 12u) : 0xFFFFFFFFu, cnext = inext;
+    uint32_t gi = gb;
+    auto issue = [&](uint32_t slot) {
+        if (gi < ge) {
+            while (inext <= gi) {
+                ++ii;
+                ir = lds128(rows + 16u * ii);
+                inext = ii + 1 < d ? lds32(rows + 16u * (ii + 1) + 12u) : 0xFFFFFFFFu;
+            }
+            const uint32_t pos = 32u * (gi - ir.w) + lane;
+            if (pos < ir.z)
+                cp_async4(ring + 128u * slot + 4u * lane,
+                          P.out_adj + ((static_cast<uint64_t>(ir.y) << 32) | ir.x) + pos);
+        }
+        cp_async_commit();
+        ++gi;
+    };
+#pragma unroll
+    for (uint32_t s = 0; s < kRing; ++s) issue(s);
+    for (uint32_t g = gb; g < ge; ++g) {
+        cp_async_wait<kRing - 1>();
+        const uint32_t slot = (g - gb) & (kRing - 1);
+        while (cnext <= g) {
+            ++ci;
+            cr = lds128(rows + 16u * ci);
+            cnext = ci + 1 < d ? lds32(rows + 16u * (ci + 1) + 12u) : 0xFFFFFFFFu;
+        }
+        const bool ok = 32u * (g - cr.w) + lane < cr.z;
+        const uint32_t y = ok ? lds32(ring + 128u * slot + 4u * lane) : kNone;
+        const bool h = probe(y, ok);
+        hits += h;
+        if constexpr (F != 0u) {
+            if (__any_sync(FULL, h)) sink.batch(h, __ldg(P.set_adj + so + ci), y);
+            if (((g - gb) & 3u) == 3u) sink.drain(P, seed);
+        }
+        issue(slot);
+    }
+    cp_async_wait<0>();
+#else
     for (uint32_t i = lo, g = gb; g < ge && i < d; ++i) {
         const uint4 r = lds128(rows + 16u * i);  // {ro lo, ro hi, len, first block}
         const uint32_t nb = (r.z + 31u) >> 5;
@@ -639,17 +724,23 @@ __device__ __forceinline__ void cta_blocks(const ListParams& P, uint32_t seed, u
                                probe, sink, hits);
         g = r.w + ke;
     }
+#endif
     sink.cnt += hits;
 }
 
-template <int ALGO, unsigned F>
-__global__ void __launch_bounds__(kCThreads, 1) k_list_hash_cta(ListParams P) {
+template <int ALGO, unsigned F, class CFG>
+__global__ void __launch_bounds__(CFG::kThreads, CFG::kMinBlocks) k_list_hash_cta(ListParams P) {
+    constexpr int kCThreads = CFG::kThreads;
+    constexpr int kCWarps = CFG::kWarps;
+    constexpr uint32_t kCMaxBits = CFG::kMaxBits;
+    constexpr uint32_t kCMaxD = CFG::kMaxD;
+    constexpr size_t kCTableBytes = cta_table_bytes<CFG>();
     extern __shared__ __align__(16) unsigned char dsm[];
     __shared__ unsigned unit, next_block, total_blocks;
     using BS = cub::BlockScan<uint32_t, kCThreads>;
     __shared__ typename BS::TempStorage scan_tmp;
     unsigned char* tbase = dsm + warp_scratch_bytes<F>(kCWarps);
-    constexpr uint32_t kSlotBytes = 16u << kCMaxBits, kWinBytes = (1u << kCWinBits) / 8;
+    constexpr uint32_t kSlotBytes = 16u << kCMaxBits, kWinBytes = kCWinBytes;
     BucketTable T{reinterpret_cast<uint32_t*>(tbase), reinterpret_cast<uint32_t*>(tbase + kSlotBytes + kWinBytes),
                   reinterpret_cast<unsigned*>(tbase + kSlotBytes + kWinBytes + kStash * 4),
                   reinterpret_cast<uint32_t*>(tbase + kSlotBytes),
@@ -705,7 +796,7 @@ __global__ void __launch_bounds__(kCThreads, 1) k_list_hash_cta(ListParams P) {
         __syncthreads();
         const uint32_t nblocks = total_blocks;
         dispatch_probe(T, shift, *T.nstash, P.set_adj + so, d, P.variant, [&](const auto& probe) {
-            cta_blocks<ALGO, F>(P, seed, so, d, rows, nblocks, probe, sink);
+            cta_blocks<ALGO, F, CFG>(P, seed, so, d, rows, nblocks, probe, sink);
         });
         sink.end_unit(P, seed);
         __syncthreads();
@@ -756,13 +847,15 @@ __global__ void __launch_bounds__(kGThreads) k_list_giant(ListParams P) {
 // dynamic shared memory per CTA of each class kernel
 template <unsigned F> constexpr size_t smem_reg() { return warp_scratch_bytes<F>(kRWarps); }
 template <unsigned F> constexpr size_t smem_hash_warp() { return warp_scratch_bytes<F>(kHWarps) + kHWarps * kHTableBytes; }
-template <unsigned F> constexpr size_t smem_hash_cta() { return warp_scratch_bytes<F>(kCWarps) + kCTableBytes + kCRowBytes; }
+template <unsigned F, class CFG> constexpr size_t smem_hash_cta() { return warp_scratch_bytes<F>(CFG::kWarps) + cta_table_bytes<CFG>() + cta_row_bytes<CFG>(); }
 template <unsigned F> constexpr size_t smem_giant() { return warp_scratch_bytes<F>(kGWarps); }
 
 // ---- seed classification --------------------------------------------------
+constexpr int kClasses = 5;  // R, H, C1, C2, G
+
 struct SeedLists {
-    uint32_t* lists[4];       // R, H, C, G
-    unsigned int* counts;     // [4]
+    uint32_t* lists[kClasses];
+    unsigned int* counts;     // [kClasses]
 };
 
 __global__ void __launch_bounds__(256) k_classify_seeds(uint32_t n, const uint64_t* __restrict__ set_off,
@@ -775,9 +868,9 @@ __global__ void __launch_bounds__(256) k_classify_seeds(uint32_t n, const uint64
         uint64_t d = 0;
         if (r < n) d = set_off[r + 1] - set_off[r];
         int cls = -1;
-        if (d >= 2) cls = d <= 32 ? 0 : d <= 256 ? 1 : d <= 4096 ? 2 : 3;
+        if (d >= 2) cls = d <= 32 ? 0 : d <= 256 ? 1 : d <= CfgC1::kMaxD ? 2 : d <= CfgC2::kMaxD ? 3 : 4;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < kClasses; ++c) {
             const unsigned b = __ballot_sync(FULL, cls == c);
             if (!b) continue;
             const unsigned leader = __ffs(b) - 1;

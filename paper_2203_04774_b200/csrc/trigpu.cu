@@ -65,7 +65,7 @@ struct tl_ctx {
     cudaEvent_t fork = nullptr, join = nullptr;
     std::string err;
     double phase_ms[PH_COUNT] = {};
-    uint64_t launches = 0;
+    uint64_t launches = 0, orient_launches = 0;
 
     uint32_t n = 0;
     uint64_t m = 0;
@@ -165,7 +165,7 @@ tl_status scan_offsets(tl_ctx* ctx, uint32_t n, const uint32_t* cnt, uint64_t* o
 
 // Segmented sort of every row of (off, adj) in place; tmp has >= off[n] slots.
 tl_status sort_rows(tl_ctx* ctx, uint32_t n, uint64_t* off, uint32_t* adj, uint32_t* tmp) {
-    ENSURE(small, 64);
+    ENSURE(small, 128);
     auto* counts = static_cast<unsigned int*>(ctx->small.p);
     CK(cudaMemsetAsync(counts, 0, 4 * sizeof(unsigned int), ctx->s));
     uint32_t* lists = P<uint32_t>(ctx->lists);
@@ -210,8 +210,8 @@ tl_status orient_core(tl_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* goff,
     ENSURE(indeg, (size_t)n * 4);
     ENSURE(out_off, ((size_t)n + 1) * 8);
     ENSURE(out_adj, m * 4 + 64);  // +16 words: bulk copies round row ends up to 16 B
-    ENSURE(lists, (size_t)n * 16);
-    ENSURE(small, 64);
+    ENSURE(lists, (size_t)n * 4 * kClasses);
+    ENSURE(small, 128);
     auto* flags = static_cast<unsigned long long*>(ctx->small.p);  // [0] err, [4..] scratch
     const unsigned big = ctx->sms * 16;
 
@@ -266,6 +266,7 @@ tl_status orient_core(tl_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* goff,
     ctx->phase_ms[PH_SORT] = ev_ms(ctx->ev[PH_SCATTER], ctx->ev[PH_SORT]);
     ctx->phase_ms[PH_COST] = ev_ms(ctx->ev[PH_SORT], ctx->ev[PH_COST]);
     ctx->orient_ms = ev_ms(ctx->ev[PH_H2D], ctx->ev[PH_COST]);
+    ctx->orient_launches = ctx->launches;
     ctx->oriented = true;
     return TL_OK;
 }
@@ -330,19 +331,33 @@ unsigned resident_grid(tl_ctx* ctx, K kernel, int threads, size_t smem) {
     return static_cast<unsigned>(per_sm * ctx->sms);
 }
 
+template <int ALGO, unsigned F, class CFG>
+tl_status launch_cta(tl_ctx* ctx, ListParams p, uint32_t* list, unsigned count, unsigned int* queue) {
+    p.seeds = list;
+    p.nseeds = count;
+    p.queue = queue;
+    const size_t smem = smem_hash_cta<F, CFG>();
+    tl_status st = set_smem(ctx, k_list_hash_cta<ALGO, F, CFG>, smem);
+    if (st != TL_OK) return st;
+    const unsigned grid = std::min<unsigned>(count, resident_grid(ctx, k_list_hash_cta<ALGO, F, CFG>, CFG::kThreads, smem));
+    k_list_hash_cta<ALGO, F, CFG><<<grid, CFG::kThreads, smem, ctx->s>>>(p);
+    LAUNCHED();
+    return TL_OK;
+}
+
 template <int ALGO, unsigned F>
-tl_status launch_classes(tl_ctx* ctx, ListParams base, uint32_t* const lists[4], const unsigned h[4],
+tl_status launch_classes(tl_ctx* ctx, ListParams base, uint32_t* const lists[kClasses], const unsigned h[kClasses],
                          unsigned int* queues) {
     tl_status st;
     // class G first, on the side stream: a few long CTAs overlap the rest
-    if (h[3]) {
+    if (h[4]) {
         ListParams p = base;
-        p.seeds = lists[3];
-        p.nseeds = h[3];
-        p.queue = queues + 3;
+        p.seeds = lists[4];
+        p.nseeds = h[4];
+        p.queue = queues + 4;
         const size_t smem = smem_giant<F>();
         if ((st = set_smem(ctx, k_list_giant<ALGO, F>, smem)) != TL_OK) return st;
-        const unsigned grid = std::min<unsigned>(h[3], (unsigned)ctx->sms);
+        const unsigned grid = std::min<unsigned>(h[4], (unsigned)ctx->sms);
         p.bitmap_words = ((uint64_t)ctx->n + 31) / 32 + 32;
         const size_t bm_bytes = (size_t)grid * p.bitmap_words * 4;
         if (ctx->bitmaps.cap < bm_bytes) {
@@ -382,22 +397,19 @@ tl_status launch_classes(tl_ctx* ctx, ListParams base, uint32_t* const lists[4],
         LAUNCHED();
     }
     if (h[2]) {
-        ListParams p = base;
-        p.seeds = lists[2];
-        p.nseeds = h[2];
-        p.queue = queues + 2;
-        const size_t smem = smem_hash_cta<F>();
-        if ((st = set_smem(ctx, k_list_hash_cta<ALGO, F>, smem)) != TL_OK) return st;
-        const unsigned grid = std::min<unsigned>(h[2], resident_grid(ctx, k_list_hash_cta<ALGO, F>, kCThreads, smem));
-        k_list_hash_cta<ALGO, F><<<grid, kCThreads, smem, ctx->s>>>(p);
-        LAUNCHED();
+        st = launch_cta<ALGO, F, CfgC1>(ctx, base, lists[2], h[2], queues + 2);
+        if (st != TL_OK) return st;
     }
-    if (h[3]) CK(cudaStreamWaitEvent(ctx->s, ctx->join, 0));
+    if (h[3]) {
+        st = launch_cta<ALGO, F, CfgC2>(ctx, base, lists[3], h[3], queues + 3);
+        if (st != TL_OK) return st;
+    }
+    if (h[4]) CK(cudaStreamWaitEvent(ctx->s, ctx->join, 0));
     return TL_OK;
 }
 
 template <int ALGO>
-tl_status launch_flags(tl_ctx* ctx, unsigned F, ListParams base, uint32_t* const lists[4], const unsigned h[4],
+tl_status launch_flags(tl_ctx* ctx, unsigned F, ListParams base, uint32_t* const lists[kClasses], const unsigned h[kClasses],
                        unsigned int* queues) {
     switch (F & 7u) {
         case 0: return launch_classes<ALGO, 0>(ctx, base, lists, h, queues);
@@ -538,14 +550,15 @@ TL_API tl_status tl_list(tl_ctx* ctx, int algo, unsigned out_flags, tl_stats* ou
         return ctx->fail(TL_ERR_INVALID_ARGUMENT, "tl_list: out-degree >= 2^27 is not supported");
     const uint32_t n = ctx->n;
     tl_status st;
+    ctx->launches = 0;  // this call's kernels; the last orient's are in orient_launches
     if (algo == TL_ALGO_APP) {
         st = ensure_in_csr(ctx);
         if (st != TL_OK) return st;
     }
     ENSURE(acc, 8 * sizeof(unsigned long long));
-    ENSURE(small, 64);
+    ENSURE(small, 128);
     auto* acc = P<unsigned long long>(ctx->acc);
-    auto* counts = static_cast<unsigned int*>(ctx->small.p);  // [0..3] class sizes, [4..7] queues
+    auto* counts = static_cast<unsigned int*>(ctx->small.p);  // [0..4] class sizes, [8..12] queues
     const bool want_vc = out_flags & TL_OUT_VERTEX_COUNTS;
     const bool want_list = out_flags & TL_OUT_LIST;
     if (want_vc) ENSURE(vcount, (size_t)n * 8);
@@ -563,26 +576,26 @@ TL_API tl_status tl_list(tl_ctx* ctx, int algo, unsigned out_flags, tl_stats* ou
     base.win_bits = ctx->win_bits;
 
     CK(cudaEventRecord(ctx->ev[PH_COUNT + 3], ctx->s));
-    CK(cudaMemsetAsync(counts, 0, 8 * sizeof(unsigned int), ctx->s));
+    CK(cudaMemsetAsync(counts, 0, 16 * sizeof(unsigned int), ctx->s));
     uint32_t* L = P<uint32_t>(ctx->lists);
-    uint32_t* const lists[4] = {L, L + n, L + 2 * (uint64_t)n, L + 3 * (uint64_t)n};
-    SeedLists SL{{lists[0], lists[1], lists[2], lists[3]}, counts};
+    uint32_t* const lists[kClasses] = {L, L + n, L + 2 * (uint64_t)n, L + 3 * (uint64_t)n, L + 4 * (uint64_t)n};
+    SeedLists SL{{lists[0], lists[1], lists[2], lists[3], lists[4]}, counts};
     if (n) {
         k_classify_seeds<<<grid_for(n, 256, ctx->sms * 16), 256, 0, ctx->s>>>(n, base.set_off, SL);
         LAUNCHED();
     }
     CK(cudaEventRecord(ctx->ev[PH_CLASSIFY], ctx->s));
-    unsigned h[4];
+    unsigned h[kClasses];
     CK(cudaMemcpyAsync(h, counts, sizeof(h), cudaMemcpyDeviceToHost, ctx->s));
     CK(cudaStreamSynchronize(ctx->s));
 
     CK(cudaEventRecord(ctx->ev[PH_COUNT + 4], ctx->s));  // listing kernels start
     auto run = [&](unsigned F) -> tl_status {
         CK(cudaMemsetAsync(acc, 0, 8 * sizeof(unsigned long long), ctx->s));
-        CK(cudaMemsetAsync(counts + 4, 0, 4 * sizeof(unsigned int), ctx->s));
+        CK(cudaMemsetAsync(counts + 8, 0, 8 * sizeof(unsigned int), ctx->s));
         if (F & F_VCOUNT) CK(cudaMemsetAsync(ctx->vcount.p, 0, (size_t)n * 8, ctx->s));
-        return algo == TL_ALGO_APM ? launch_flags<ALGO_APM>(ctx, F, base, lists, h, counts + 4)
-                                   : launch_flags<ALGO_APP>(ctx, F, base, lists, h, counts + 4);
+        return algo == TL_ALGO_APM ? launch_flags<ALGO_APM>(ctx, F, base, lists, h, counts + 8)
+                                   : launch_flags<ALGO_APP>(ctx, F, base, lists, h, counts + 8);
     };
     unsigned long long res[3] = {0, 0, 0};
     if (want_list) {
@@ -620,7 +633,7 @@ TL_API tl_status tl_list(tl_ctx* ctx, int algo, unsigned out_flags, tl_stats* ou
         out->orient_ms = ctx->orient_ms;
         out->list_ms = ev_ms(ctx->ev[PH_COUNT + 3], ctx->ev[PH_LIST]);
         out->h2d_ms = ctx->h2d_ms;
-        out->kernel_launches = ctx->launches;
+        out->kernel_launches = ctx->orient_launches + ctx->launches;
     }
     return TL_OK;
 }
