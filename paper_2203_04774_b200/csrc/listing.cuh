@@ -60,7 +60,7 @@ struct ListParams {
 // Per-warp hit buffer: hits (x, y) are compacted into shared memory by a
 // ballot and emitted 32 at a time with every lane busy, instead of running
 // the dense-id gathers / hash / atomics with the 1-3 lanes that hit in a batch.
-constexpr int kHitBuf = 160;  // 31 pending + up to 4 batches of 32 before a drain
+constexpr int kHitBuf = 96;  // 31 pending + up to 2 batches of 32 before a drain
 // 32-element blocks loaded per warp before probing (memory-level parallelism):
 // the count-only sink keeps more in flight than the sinks that buffer hits
 constexpr int kUnrollCount = 16;
@@ -144,7 +144,7 @@ struct Sink {
         }
     }
 
-    // Emit every full group of 32 buffered hits (call after <= 4 batches).
+    // Emit every full group of 32 buffered hits (call after <= 2 batches).
     __device__ __forceinline__ void drain(const ListParams& P, uint32_t seed) {
         if constexpr (F != 0u) {
             if (pending < 32) return;
@@ -225,7 +225,7 @@ __device__ __forceinline__ void stream_blocks(const ListParams& P, uint32_t seed
 #pragma unroll
                 for (int i = 0; i < U; ++i) {
                     sink.batch(h[i], x, y[i]);
-                    if (i % 4 == 3) sink.drain(P, seed);
+                    if (i % 2 == 1) sink.drain(P, seed);
                 }
             }
         }
@@ -635,7 +635,7 @@ struct CtaCfg {
     static constexpr uint32_t kMaxD = MAXD;
     static constexpr int kMinBlocks = MINB;
 };
-using CfgC1 = CtaCfg<256, 11, 1024, 3>;
+using CfgC1 = CtaCfg<256, 11, 1024, 4>;
 using CfgC2 = CtaCfg<1024, 12, 4096, 1>;
 constexpr uint32_t kCBatch = 4;
 constexpr uint32_t kCWinBits = 18;  // 262144-rank window = 32 KB
@@ -708,7 +708,7 @@ __device__ __forceinline__ void cta_blocks(const ListParams& P, uint32_t seed, u
         hits += h;
         if constexpr (F != 0u) {
             if (__any_sync(FULL, h)) sink.batch(h, __ldg(P.set_adj + so + ci), y);
-            if (((g - gb) & 3u) == 3u) sink.drain(P, seed);
+            if (((g - gb) & 1u) == 1u) sink.drain(P, seed);
         }
         issue(slot);
     }
