@@ -35,11 +35,11 @@ $(LIB)/libtrigpu.so: $(CU_SRCS) $(CU_HDRS)
 	@mkdir -p $(LIB)
 	$(NVCC) $(NVFLAGS) -Xptxas -v -shared $(CU_SRCS) -o $@ -lcudart_static -lrt -ldl -lpthread 2> build_ptxas.log || (cat build_ptxas.log; exit 1)
 
-# experimental build with the hub-window probe (A/B timing via TRIGPU_LIB_SUFFIX=_win)
-gpu_win: $(LIB)/libtrigpu_win.so
-$(LIB)/libtrigpu_win.so: $(CU_SRCS) $(CU_HDRS)
+# experimental build (TRIGPU_VARIANT=2: null probe) for A/B timing via TRIGPU_LIB_SUFFIX=_exp
+gpu_exp: $(LIB)/libtrigpu_exp.so
+$(LIB)/libtrigpu_exp.so: $(CU_SRCS) $(CU_HDRS)
 	@mkdir -p $(LIB)
-	$(NVCC) $(NVFLAGS) -DTRIGPU_HUB_WINDOW -DTRIGPU_EXPERIMENTS -shared $(CU_SRCS) -o $@ -lcudart_static -lrt -ldl -lpthread
+	$(NVCC) $(NVFLAGS) -DTRIGPU_EXPERIMENTS -shared $(CU_SRCS) -o $@ -lcudart_static -lrt -ldl -lpthread
 
 $(LIB)/libtrihost.so: $(CSRC)/host/trihost.cpp $(CSRC)/host/trihost.h $(REF_HOST_SRCS)
 	@mkdir -p $(LIB)

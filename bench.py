@@ -309,7 +309,7 @@ def reference_arm(args, cfg, world, rank):
 
 def config_block(args, cfg, g):
     return {"workload": args.config, "desc": cfg["desc"], "n": g.n, "m": g.m,
-            "ordering": args.ordering, "algo": "apm", "sinks": "count+checksum",
+            "ordering": args.ordering, "algo": args.algo, "sinks": args.sinks,
             "step": "tl_orient (relabel+orient+CSR+segsort+cost) + tl_list (A+-)",
             "l2": "inputs larger than L2 (adjacency %.1f GB vs 126 MB L2)" % (8 * g.m / 1e9)}
 
@@ -317,7 +317,7 @@ def config_block(args, cfg, g):
 def trigpu_arm(args, cfg, world, rank, local):
     import torch
     import paper_2203_04774_b200 as tg
-    from paper_2203_04774_b200._native import TL_ALGO_APM, TL_OUT_CHECKSUM
+    from paper_2203_04774_b200._native import TL_ALGO_APM, TL_ALGO_APP, TL_OUT_CHECKSUM, TL_OUT_VERTEX_COUNTS
 
     t0 = time.perf_counter()
     g = make_graph(cfg)
@@ -327,7 +327,9 @@ def trigpu_arm(args, cfg, world, rank, local):
     log(f"[bench] {args.ordering} ordering: {order_ms:.1f} ms (+ reference Graph build, "
         f"{time.perf_counter() - t0:.1f}s total)")
     ctx = tg.Context(local)
-    flags = TL_OUT_CHECKSUM
+    flags = {"count": 0, "count+checksum": TL_OUT_CHECKSUM,
+             "count+checksum+vcounts": TL_OUT_CHECKSUM | TL_OUT_VERTEX_COUNTS}[args.sinks]
+    ALGO = TL_ALGO_APM if args.algo == "apm" else TL_ALGO_APP
 
     # --- device-resident inputs -------------------------------------------------
     torch.cuda.set_device(local)
@@ -338,12 +340,12 @@ def trigpu_arm(args, cfg, world, rank, local):
 
     def step_device():
         ctx.orient_device(g.n, g.m, d_off.data_ptr(), d_adj.data_ptr(), d_rank.data_ptr())
-        return ctx.list(TL_ALGO_APM, flags)
+        return ctx.list(ALGO, flags)
 
     for _ in range(args.warmup):
         st = step_device()
     T = int(st.triangle_count)
-    C_pm = int(st.c_pm)
+    C_pm = int(st.inner_ops)  # c_pm (A+-) or c_pp (A++)
     B_list = 4 * (C_pm + 2 * g.m)  # 4 * (inner_ops + mark_ops)
 
     sampler = ClockSampler(local)
@@ -373,13 +375,13 @@ def trigpu_arm(args, cfg, world, rank, local):
     ctx.host_register(pi.ranks)
     for _ in range(max(1, args.warmup)):
         ctx.orient(g.offsets, g.adjacency, pi.ranks)
-        ctx.list(TL_ALGO_APM, flags)
+        ctx.list(ALGO, flags)
     barrier(world)
     t0 = time.perf_counter()
     h2d_ms = []
     for _ in range(args.steps):
         ctx.orient(g.offsets, g.adjacency, pi.ranks)
-        st = ctx.list(TL_ALGO_APM, flags)  # stats read back (D2H) inside
+        st = ctx.list(ALGO, flags)  # stats read back (D2H) inside
         assert int(st.triangle_count) == T
         h2d_ms.append(float(st.h2d_ms))
     e2e_s = allreduce_max(time.perf_counter() - t0, world)
@@ -428,7 +430,7 @@ def trigpu_arm(args, cfg, world, rank, local):
         "phase_ms": ph,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "listing kernels (k_list_reg/hash_warp/hash_cta/giant)",
+                     "kernel": "listing kernels (k_list_reg/warp/cta/giant)",
                      "algorithmic_bytes": B_list, "peak_source": peak_src,
                      "frac_of_8TBs_nominal": achieved / 8000.0},
         "cpu_baseline": cpu,
@@ -450,6 +452,8 @@ def main():
     ap.add_argument("--impl", default="trigpu", choices=["trigpu", "reference"])
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--ordering", default="degree")
+    ap.add_argument("--algo", default="apm", choices=["apm", "app"])
+    ap.add_argument("--sinks", default="count+checksum", choices=["count", "count+checksum", "count+checksum+vcounts"])
     ap.add_argument("--ref-budget", type=float, default=10.0, help="seconds of reference work per sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

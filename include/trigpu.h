@@ -71,7 +71,7 @@ typedef struct {
     uint64_t inner_ops; /* = c_pp (app) or c_pm (apm) */
     uint64_t mark_ops;  /* = 2m */
     /* extensions */
-    uint64_t checksum;  /* sum mod 2^64 of mix64 chain over dense-id-sorted triples */
+    uint64_t checksum;  /* sum mod 2^64 over triangles of h(a) h(b) h(c), h(v) = mix64(v) | 1, dense ids */
     uint64_t c_pp, c_pm, c_mm, sum_deg_sq; /* CostReport (cost.hpp:15-20) */
     double orient_ms;   /* device time of the last tl_orient (relabel+CSR+sort) */
     double list_ms;     /* device time of the listing kernels (ListingStats::wall_ms analogue) */

@@ -25,12 +25,10 @@ uint64_t or_mix64(uint64_t z) {
     return z ^ (z >> 31);
 }
 
+uint64_t or_vertex_hash(uint32_t v) { return or_mix64(v) | 1u; }
+
 uint64_t or_triangle_hash(uint32_t a, uint32_t b, uint32_t c) {
-    uint32_t t;
-    if (a > b) { t = a; a = b; b = t; }
-    if (b > c) { t = b; b = c; c = t; }
-    if (a > b) { t = a; a = b; b = t; }
-    return or_mix64(or_mix64(or_mix64(a) ^ b) ^ c);
+    return or_vertex_hash(a) * or_vertex_hash(b) * or_vertex_hash(c);
 }
 
 /* oriented_view.cpp:7-47: count pass (:18-26), prefix sums (:27-30), then a

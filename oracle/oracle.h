@@ -34,9 +34,11 @@ typedef struct {
 
 /* splitmix64 finaliser. */
 uint64_t or_mix64(uint64_t z);
-/* Hash of one triangle: ids sorted ascending (dense ids), then
- * mix64(mix64(mix64(a) ^ b) ^ c). The checksum is the wrapping sum of this
- * over all triangles. */
+/* Vertex hash h(v) = mix64(v) | 1 (odd, so products never vanish). */
+uint64_t or_vertex_hash(uint32_t v);
+/* Hash of one triangle over DENSE ids: h(a) * h(b) * h(c) mod 2^64 --
+ * symmetric, so no sort and no orientation dependence. The checksum is the
+ * wrapping sum of this over all triangles. */
 uint64_t or_triangle_hash(uint32_t a, uint32_t b, uint32_t c);
 
 /* OrientedView(g, pi) (reference oriented_view.cpp:7-47): dense-id CSR with

@@ -44,11 +44,11 @@ std::uint64_t mix64(std::uint64_t z) {
     return z ^ (z >> 31);
 }
 
+// h(a) * h(b) * h(c) mod 2^64, h(v) = mix64(v) | 1 (symmetric: no sort)
+std::uint64_t vertex_hash(VertexId v) { return mix64(v) | 1u; }
+
 std::uint64_t triangle_hash(VertexId a, VertexId b, VertexId c) {
-    if (a > b) std::swap(a, b);
-    if (b > c) std::swap(b, c);
-    if (a > b) std::swap(a, b);
-    return mix64(mix64(mix64(a) ^ b) ^ c);
+    return vertex_hash(a) * vertex_hash(b) * vertex_hash(c);
 }
 
 // Which outputs HarnessSink records; set once per ref_list call (the harness

@@ -17,15 +17,13 @@ __host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
     return z ^ (z >> 31);
 }
 
-// Order-independent triangle hash over DENSE ids: sort the triple, then
-// mix64(mix64(mix64(a) ^ b) ^ c).
+// Order-independent triangle hash over DENSE ids: h(a) * h(b) * h(c) mod
+// 2^64 with the odd vertex hash h(v) = mix64(v) | 1. Symmetric, so the device
+// never sorts, and it factors: the checksum of all triangles (s, x, y) of one
+// row is h(s) h(x) * sum_y h(y) -- one 64-bit multiply per row chunk.
+__host__ __device__ __forceinline__ uint64_t vertex_hash(uint32_t v) { return mix64(v) | 1ull; }
 __host__ __device__ __forceinline__ uint64_t tri_hash(uint32_t a, uint32_t b, uint32_t c) {
-    uint32_t lo = a < b ? a : b, hi = a < b ? b : a;
-    uint32_t mid;
-    if (c < lo) { mid = lo; lo = c; }
-    else if (c > hi) { mid = hi; hi = c; }
-    else mid = c;
-    return mix64(mix64(mix64(lo) ^ mid) ^ hi);
+    return vertex_hash(a) * vertex_hash(b) * vertex_hash(c);
 }
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
@@ -128,6 +126,42 @@ __device__ __forceinline__ void ldg4(const uint32_t* const (&a)[4], uint32_t (&v
         : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
         : "l"(a[0]), "l"(a[1]), "l"(a[2]), "l"(a[3]));
 }
+
+// Four predicated 16-byte read-only loads in ONE asm block (all four in
+// flight before any use); a lane whose predicate is off keeps its old values.
+__device__ __forceinline__ void ldg4q(const uint4* const (&a)[4], const bool (&p)[4], uint4 (&v)[4]) {
+    asm volatile(
+        "{\n\t.reg .pred q0, q1, q2, q3;\n\t"
+        "setp.ne.u32 q0, %16, 0;\n\t"
+        "setp.ne.u32 q1, %17, 0;\n\t"
+        "setp.ne.u32 q2, %18, 0;\n\t"
+        "setp.ne.u32 q3, %19, 0;\n\t"
+        "@q0 ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%20];\n\t"
+        "@q1 ld.global.nc.v4.u32 {%4, %5, %6, %7}, [%21];\n\t"
+        "@q2 ld.global.nc.v4.u32 {%8, %9, %10, %11}, [%22];\n\t"
+        "@q3 ld.global.nc.v4.u32 {%12, %13, %14, %15}, [%23];\n\t"
+        "}"
+        : "+r"(v[0].x), "+r"(v[0].y), "+r"(v[0].z), "+r"(v[0].w), "+r"(v[1].x), "+r"(v[1].y), "+r"(v[1].z),
+          "+r"(v[1].w), "+r"(v[2].x), "+r"(v[2].y), "+r"(v[2].z), "+r"(v[2].w), "+r"(v[3].x), "+r"(v[3].y),
+          "+r"(v[3].z), "+r"(v[3].w)
+        : "r"((unsigned)p[0]), "r"((unsigned)p[1]), "r"((unsigned)p[2]), "r"((unsigned)p[3]), "l"(a[0]), "l"(a[1]),
+          "l"(a[2]), "l"(a[3]));
+}
+
+__device__ __forceinline__ void ldg2q(const uint4* const (&a)[2], const bool (&p)[2], uint4 (&v)[2]) {
+    asm volatile(
+        "{\n\t.reg .pred q0, q1;\n\t"
+        "setp.ne.u32 q0, %8, 0;\n\t"
+        "setp.ne.u32 q1, %9, 0;\n\t"
+        "@q0 ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%10];\n\t"
+        "@q1 ld.global.nc.v4.u32 {%4, %5, %6, %7}, [%11];\n\t"
+        "}"
+        : "+r"(v[0].x), "+r"(v[0].y), "+r"(v[0].z), "+r"(v[0].w), "+r"(v[1].x), "+r"(v[1].y), "+r"(v[1].z),
+          "+r"(v[1].w)
+        : "r"((unsigned)p[0]), "r"((unsigned)p[1]), "l"(a[0]), "l"(a[1]));
+}
+__device__ __forceinline__ void ldgq(const uint4* const (&a)[4], const bool (&p)[4], uint4 (&v)[4]) { ldg4q(a, p, v); }
+__device__ __forceinline__ void ldgq(const uint4* const (&a)[2], const bool (&p)[2], uint4 (&v)[2]) { ldg2q(a, p, v); }
 
 // Ampere-style asynchronous 4-byte copies global -> shared (LDGSTS): the
 // data in flight lives in shared memory, not in registers.

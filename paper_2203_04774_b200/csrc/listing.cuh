@@ -9,17 +9,16 @@
 // when y in S". All ids are ranks, rows ascending. The triangle is
 // (s, x, y) for A+- and (x, y, s) for A++ - already rank-ascending.
 //
-// The reference's uint8 table[n] becomes a per-seed probe structure sized to
-// |S| (degree binning):
-//   class R  2 <= |S| <= 32     warp per seed, S in registers (one id per lane),
-//                               membership by a 5-step shuffle binary search
-//   class H  32 < |S| <= 256    warp per seed, per-warp shared-memory hash
-//   class C  256 < |S| <= 4096  CTA per (seed, x-slice), shared-memory hash
-//   class G  |S| > 4096         CTA per seed, per-CTA global bitmap over ranks
-// Every class walks the rows of 32 x's at a time as ONE flattened, coalesced
-// stream (lane f of a batch reads element f of the concatenated rows; the row
-// of each lane is found from a warp OR-reduction of row starts), so short
-// rows do not idle lanes.
+// The reference's uint8 table[n] (listing.hpp:113) becomes a per-seed
+// windowed bitmap in shared memory sized to the class of |S| (degree binning):
+//   class R  2 <= |S| <= 32     warp per seed, 2^13-bit window per warp
+//   class H  32 < |S| <= 256    warp per seed, 2^15-bit window per warp
+//   class C1 256 < |S| <= 1024  CTA (8 warps) per seed, 2^18-bit window
+//   class C2 1024 < |S| <= 4096 CTA (32 warps) per seed, 2^19-bit window
+//   class G  |S| > 4096         CTA per seed, n-bit bitmap in global memory
+// Every class reads the out-rows of the seed's set as 128-element chunks of
+// 16-byte quads (one 512-byte warp load per chunk, four chunks in flight);
+// rows shorter than kLongRow are walked as one flattened stream over 32 rows.
 //
 // Sinks are fused into the same pass (template flags): count, order-
 // independent checksum over dense ids, per-vertex counts, and list output by
@@ -44,6 +43,7 @@ struct ListParams {
     const uint64_t* out_off;  // scanned rows: always the out-CSR
     const uint32_t* out_adj;
     const uint32_t* inv;      // rank -> dense id
+    const unsigned long long* hv;  // rank -> vertex_hash(dense id) (checksum sink)
     unsigned long long* acc;  // [0] triangles, [1] checksum, [2] list cursor
     unsigned long long* vcount;  // rank space
     uint32_t* tri;
@@ -53,104 +53,233 @@ struct ListParams {
     unsigned int* queue;      // dynamic work counter
     uint32_t* bitmaps;        // class G only: one n-bit bitmap per CTA
     uint64_t bitmap_words;
-    int variant;              // reserved for A/B probe experiments
-    uint32_t win_bits;        // hub-window size (log2 ranks, capped per class); 0 = no window
+    int variant;              // TRIGPU_VARIANT: 2 = null probe (timing experiments only)
+    uint32_t bm_shrink;       // TRIGPU_BM_SHRINK: smaller windows (tests force the below-window path)
 };
 
-// Per-warp hit buffer: hits (x, y) are compacted into shared memory by a
-// ballot and emitted 32 at a time with every lane busy, instead of running
-// the dense-id gathers / hash / atomics with the 1-3 lanes that hit in a batch.
+// Per-warp hit buffer (per-vertex-count and list sinks): hits (x, y) are
+// compacted into shared memory by a ballot and emitted 32 at a time with
+// every lane busy (dense-id gathers, atomics) instead of with the 1-3 lanes
+// that hit in a batch.
 constexpr int kHitBuf = 96;  // 31 pending + up to 2 batches of 32 before a drain
-// 32-element blocks loaded per warp before probing (memory-level parallelism):
-// the count-only sink keeps more in flight than the sinks that buffer hits
-constexpr int kUnrollCount = 16;
-constexpr int kUnrollSink = 8;
-constexpr int kMetaBytes = 768;  // per warp: uint4[32] block table, u32[32] edge lanes, u32[32] x
 
-// Emit n (<= 32) buffered hits, lane i taking entry i; returns this lane's
-// checksum contribution. Out of line: it runs once per 32 triangles.
+// ---- the probe: a windowed bitmap over the seed's set ----------------------
+// S (sorted ranks s_0 < ... < s_{d-1}) is held in shared memory as
+//   region A: an EXACT bitmap over the rank window [wb, wb + LA) - one bit per
+//             rank, then one always-zero guard word;
+//   region B: for the keys below the window (only when the set spans more
+//             than LA ranks), a 2^KB-bit filter indexed by key mod 2^KB.
+// wb = s_0 when the set fits the window (no region B), else
+// wb = s_{d-1} + 1 - LA, so the window holds the set's TOP ranks: under
+// degree order the scanned rows are made of hubs, so on R-MAT 100 % of the
+// class H / C hits and >98 % of the probes fall in the window.
+// A probe of y is ONE LDS.32 of the word of bit min(y - wb, LA) (offsets
+// outside the window clamp onto the guard word). Rows are sorted, so the 32
+// lanes of a chunk read few distinct words in distinct banks: ~1.3 shared
+// wavefronts per 32 probes against ~9 for a 16-byte hash bucket.
+// Elements below the window (rare; a chunk's are found by one compare per
+// lane on its sorted quad) take region B; its candidates are verified exactly
+// (V: binary search of the sorted set) on the spot and become ordinary hits,
+// so the sinks only ever see exact hits.
+template <bool kLow, class V>
+struct WinProbe {
+    static constexpr bool low = kLow;
+    unsigned bm;     // shared address of region A
+    unsigned bmb;    // shared address of region B
+    uint32_t wb;     // window base
+    uint32_t la;     // window length LA (a power of two)
+    uint32_t maskb;  // 2^KB - 1
+    V ver;
+    // 0/1: y is in S (y inside the window) / 0 (y outside)
+    __device__ __forceinline__ uint32_t bit(uint32_t y) const {
+        const uint32_t o = min(y - wb, la);
+        return (lds32(bm + ((o >> 5) << 2)) >> (o & 31u)) & 1u;
+    }
+    __device__ __forceinline__ bool below(uint32_t y) const { return y < wb; }
+    // region-B candidate (call for y below the window only)
+    __device__ __forceinline__ uint32_t cand(uint32_t y) const {
+        const uint32_t o = y & maskb;
+        return (lds32(bmb + ((o >> 5) << 2)) >> (o & 31u)) & 1u;
+    }
+    __device__ __forceinline__ bool verify(uint32_t y, bool act) const { return ver(y, act); }
+    // the value padding a partial quad: never in the window, never below it
+    // (tl_orient keeps n <= 2^32 - 2^20, so kNone - wb >= LA)
+    __device__ __forceinline__ uint32_t sentinel() const { return kNone; }
+};
+
+// Bitmap geometry of one seed: window length, region-B mask, base.
+struct WinGeom {
+    uint32_t la, maskb, wb;
+    bool low;
+};
+__device__ __forceinline__ WinGeom win_geom(uint32_t bits_a, uint32_t bits_b, uint32_t shrink, uint32_t s0,
+                                            uint32_t top) {
+    const uint32_t ka = bits_a > shrink + 5u ? bits_a - shrink : 5u;
+    const uint32_t kb = bits_b > shrink + 5u ? bits_b - shrink : 5u;
+    WinGeom g;
+    g.la = 1u << ka;
+    g.maskb = (1u << kb) - 1u;
+    g.low = top - s0 >= g.la;
+    g.wb = g.low ? top + 1u - g.la : s0;
+    return g;
+}
+__device__ __forceinline__ void win_set(uint32_t* bma, uint32_t* bmb, const WinGeom& g, uint32_t key) {
+    if (key >= g.wb) {
+        const uint32_t o = key - g.wb;
+        atomicOr(bma + (o >> 5), 1u << (o & 31u));
+    } else {
+        const uint32_t o = key & g.maskb;
+        atomicOr(bmb + (o >> 5), 1u << (o & 31u));
+    }
+}
+__device__ __forceinline__ void win_clear(uint32_t* bma, uint32_t* bmb, const WinGeom& g, uint32_t key) {
+    if (key >= g.wb) bma[(key - g.wb) >> 5] = 0u;
+    else bmb[(key & g.maskb) >> 5] = 0u;
+}
+constexpr size_t win_bytes(uint32_t bits_a, uint32_t bits_b) {
+    return (size_t{1} << bits_a) / 8 + 16 + (size_t{1} << bits_b) / 8;  // A, guard (padded), B
+}
+
+// Exact membership for region-B candidates.
+struct RegVerify {  // S sorted ascending, one key per lane, padded with kNone (warp-collective)
+    uint32_t s;
+    __device__ __forceinline__ bool operator()(uint32_t y, bool act) const {
+        int pos = 0;
+#pragma unroll
+        for (int step = 16; step; step >>= 1) {
+            const uint32_t v = __shfl_sync(FULL, s, pos + step - 1);
+            if (v < y) pos += step;
+        }
+        const uint32_t v = __shfl_sync(FULL, s, pos & 31);
+        return act && pos < 32 && v == y && y != kNone;  // kNone pads the lanes past |S|
+    }
+};
+
+struct RowVerify {  // branch-free binary search of the seed's sorted set row (L1-resident)
+    const uint32_t* row;
+    uint32_t d;
+    __device__ __forceinline__ bool operator()(uint32_t y, bool act) const {
+        uint32_t lo = 0, len = d;
+        while (len > 1) {  // uniform trip count: log2(d) steps
+            const uint32_t half = len >> 1;
+            if (__ldg(row + lo + half) <= y) lo += half;
+            len -= half;
+        }
+        return act && __ldg(row + lo) == y;
+    }
+};
+
+// Class G: exact n-bit bitmap in global memory (L2-resident per CTA).
+struct BitmapProbe {
+    static constexpr bool low = false;
+    const uint32_t* bm;
+    uint32_t n;  // bits n .. are the always-zero slack words
+    __device__ __forceinline__ uint32_t bit(uint32_t y) const { return (__ldcg(bm + (y >> 5)) >> (y & 31)) & 1u; }
+    __device__ __forceinline__ bool below(uint32_t) const { return false; }
+    __device__ __forceinline__ uint32_t cand(uint32_t) const { return 0u; }
+    __device__ __forceinline__ bool verify(uint32_t, bool act) const { return act; }
+    __device__ __forceinline__ uint32_t sentinel() const { return n; }
+};
+
+// Timing-only probe (TRIGPU_VARIANT=2 in a -DTRIGPU_EXPERIMENTS build):
+// touches every loaded element, never hits. Measures the row-streaming limit.
+struct NullProbe {
+    static constexpr bool low = false;
+    __device__ __forceinline__ uint32_t bit(uint32_t y) const { return y == 0xFFFFFFFEu; }
+    __device__ __forceinline__ bool below(uint32_t) const { return false; }
+    __device__ __forceinline__ uint32_t cand(uint32_t) const { return 0u; }
+    __device__ __forceinline__ bool verify(uint32_t, bool act) const { return act; }
+    __device__ __forceinline__ uint32_t sentinel() const { return 0u; }
+};
+
+// Exact hit of one element, region-B candidates verified on the spot
+// (warp-convergent: RegVerify shuffles).
+template <class Probe>
+__device__ __forceinline__ bool probe_one(const Probe& probe, uint32_t y, bool act) {
+    bool hit = act && probe.bit(y);
+    if constexpr (Probe::low) {
+        const bool c = act && probe.below(y) && probe.cand(y);
+        if (__any_sync(FULL, c)) hit |= probe.verify(y, c);
+    }
+    return hit;
+}
+
+// ---- sinks -------------------------------------------------------------------
+// Count: hit bits are added in the stream. Checksum: sum over triangles
+// (s, x, y) of h(s) h(x) h(y) (common.cuh), h from the per-rank table hv; with
+// the count + checksum sinks nothing is buffered: a chunk's hits add their
+// h(y) lane-locally and one multiply by h(s) h(x) folds them in (kFastSum).
+// Per-vertex counts and lists go through the warp's hit buffer (emit).
 template <int ALGO, unsigned F>
-__device__ __forceinline__ unsigned long long emit_hits(const ListParams& P, uint32_t seed, unsigned n,
-                                                     unsigned from) {
-    const unsigned lane = lane_id();
-    const bool hit = lane < n;
-    const uint2 e = hit ? lds64(from + 8u * lane) : make_uint2(0, 0);
-    const uint32_t x = e.x, y = e.y;
-    unsigned long long sum = 0;
-    if constexpr ((F & F_VCOUNT) != 0u) {
-        if (hit) {
-            atomicAdd(&P.vcount[x], 1ull);
-            atomicAdd(&P.vcount[y], 1ull);
+struct Sink {
+    static constexpr bool kFastSum = (F & F_CHECKSUM) != 0u && (F & (F_VCOUNT | F_LIST)) == 0u;
+    static constexpr bool kBuffered = (F & (F_VCOUNT | F_LIST)) != 0u;
+    unsigned long long cnt = 0, sum = 0;
+    unsigned long long hs = 0;  // h(seed)
+    unsigned seed_hits = 0;
+    unsigned buf = 0;      // shared address of this warp's kHitBuf uint2 entries
+    unsigned pending = 0;  // warp-uniform
+
+    __device__ __forceinline__ void begin_unit(const ListParams& P, uint32_t seed) {
+        if constexpr ((F & F_CHECKSUM) != 0u) hs = __ldg(P.hv + seed);
+    }
+
+    // One hit with its own x (short-row stream), kFastSum only.
+    __device__ __forceinline__ void direct(const ListParams& P, bool hit, uint32_t x, uint32_t y) {
+        if constexpr (kFastSum)
+            if (hit) sum += hs * __ldg(P.hv + x) * __ldg(P.hv + y);
+    }
+
+    // One 32-wide batch of hits (called convergently by the warp), kBuffered only.
+    __device__ __forceinline__ void batch(bool hit, uint32_t x, uint32_t y) {
+        if constexpr (kBuffered) {
+            const unsigned b = __ballot_sync(FULL, hit);
+            if (!b) return;
+            if (hit) sts64(buf + 8u * (pending + __popc(b & lanemask_lt())), make_uint2(x, y));
+            pending += __popc(b);
         }
     }
-    if constexpr ((F & (F_CHECKSUM | F_LIST)) != 0u) {
-        const uint32_t ru = ALGO == ALGO_APM ? seed : x;
-        const uint32_t rv = ALGO == ALGO_APM ? x : y;
-        const uint32_t rw = ALGO == ALGO_APM ? y : seed;
-        uint32_t du = 0, dv = 0, dw = 0;
-        if (hit) {
-            du = __ldg(P.inv + ru);
-            dv = __ldg(P.inv + rv);
-            dw = __ldg(P.inv + rw);
+
+    // Handle n (<= 32) buffered hits, lane i taking entry i.
+    __device__ __forceinline__ void emit(const ListParams& P, uint32_t seed, unsigned n, unsigned from) {
+        const unsigned lane = lane_id();
+        const bool hit = lane < n;
+        const uint2 e = hit ? lds64(from + 8u * lane) : make_uint2(0, 0);
+        const uint32_t x = e.x, y = e.y;
+        if constexpr ((F & F_VCOUNT) != 0u) {
+            if (hit) {
+                atomicAdd(&P.vcount[x], 1ull);
+                atomicAdd(&P.vcount[y], 1ull);
+                ++seed_hits;
+            }
         }
         if constexpr ((F & F_CHECKSUM) != 0u)
-            if (hit) sum = tri_hash(du, dv, dw);
+            if (hit) sum += hs * __ldg(P.hv + x) * __ldg(P.hv + y);
         if constexpr ((F & F_LIST) != 0u) {
+            const uint32_t ru = ALGO == ALGO_APM ? seed : x;
+            const uint32_t rv = ALGO == ALGO_APM ? x : y;
+            const uint32_t rw = ALGO == ALGO_APM ? y : seed;
             unsigned long long base = 0;
             if (lane == 0) base = atomicAdd(&P.acc[2], (unsigned long long)n);
             base = __shfl_sync(FULL, base, 0);
             if (hit) {
                 const unsigned long long k = base + lane;
                 if (k < P.tri_cap) {
-                    P.tri[3 * k] = du;
-                    P.tri[3 * k + 1] = dv;
-                    P.tri[3 * k + 2] = dw;
+                    P.tri[3 * k] = __ldg(P.inv + ru);
+                    P.tri[3 * k + 1] = __ldg(P.inv + rv);
+                    P.tri[3 * k + 2] = __ldg(P.inv + rw);
                 }
             }
-        }
-    }
-    return sum;
-}
-
-template <int ALGO, unsigned F>
-struct Sink {
-    unsigned long long cnt = 0, sum = 0;
-    unsigned seed_hits = 0;
-    unsigned buf = 0;      // shared address of this warp's kHitBuf uint2 entries
-    unsigned meta = 0;     // (unused)
-    unsigned ring = 0;     // shared address of this warp's cp.async ring (kRing x 128 B)
-    unsigned pending = 0;  // warp-uniform
-
-    // One 32-wide batch (called convergently by the whole warp).
-    __device__ __forceinline__ void batch(bool hit, uint32_t x, uint32_t y) {
-        if constexpr (F != 0u) {
-            const unsigned b = __ballot_sync(FULL, hit);
-            if (!b) return;
-            if constexpr ((F & F_VCOUNT) != 0u) seed_hits += hit;
-            if (hit) sts64(buf + 8u * (pending + __popc(b & lanemask_lt())), make_uint2(x, y));
-            pending += __popc(b);
-        }
-    }
-
-    // Same, with x read (broadcast) from shared memory only if some lane hit.
-    __device__ __forceinline__ void batch_lazy(bool hit, unsigned xaddr, uint32_t y) {
-        if constexpr (F != 0u) {
-            const unsigned b = __ballot_sync(FULL, hit);
-            if (!b) return;
-            const uint32_t x = lds32(xaddr);
-            if constexpr ((F & F_VCOUNT) != 0u) seed_hits += hit;
-            if (hit) sts64(buf + 8u * (pending + __popc(b & lanemask_lt())), make_uint2(x, y));
-            pending += __popc(b);
         }
     }
 
     // Emit every full group of 32 buffered hits (call after <= 2 batches).
     __device__ __forceinline__ void drain(const ListParams& P, uint32_t seed) {
-        if constexpr (F != 0u) {
+        if constexpr (kBuffered) {
             if (pending < 32) return;
             __syncwarp();
             unsigned done = 0;
-            for (; pending - done >= 32; done += 32) sum += emit_hits<ALGO, F>(P, seed, 32, buf + 8u * done);
+            for (; pending - done >= 32; done += 32) emit(P, seed, 32, buf + 8u * done);
             __syncwarp();
             if (lane_id() < pending - done) sts64(buf + 8u * lane_id(), lds64(buf + 8u * (done + lane_id())));
             __syncwarp();
@@ -160,11 +289,11 @@ struct Sink {
 
     // End of one seed's unit: drain the buffer, credit the seed's own count.
     __device__ __forceinline__ void end_unit(const ListParams& P, uint32_t seed) {
-        if constexpr (F != 0u) {
+        if constexpr (kBuffered) {
             drain(P, seed);
             if (pending) {
                 __syncwarp();
-                sum += emit_hits<ALGO, F>(P, seed, pending, buf);
+                emit(P, seed, pending, buf);
                 __syncwarp();
                 pending = 0;
             }
@@ -186,68 +315,244 @@ struct Sink {
     }
 };
 
-// Probe the elements of blocks [kb, ke) of one row (base rp, len elements;
-// block k = elements 32k .. 32k+31, lane l takes element 32k + l): four
-// blocks' loads issued back to back, then probed; the row end is predicated.
-#ifndef TRIGPU_STREAM_U
-#define TRIGPU_STREAM_U 4
-#endif
-__device__ __forceinline__ void ldg_batch(const uint32_t* const (&a)[4], uint32_t (&y)[4]) { ldg4(a, y); }
-__device__ __forceinline__ void ldg_batch(const uint32_t* const (&a)[8], uint32_t (&y)[8]) { ldg8(a, y); }
+// ---- row streaming -------------------------------------------------------------
+// Long rows are read as 128-element CHUNKS of 16-byte quads: lane l loads
+// quad qb + l (ld.global.nc.v4: four elements), a warp load is 512 contiguous
+// bytes, and four chunks' loads are issued back to back in one asm block
+// (ldg4q), so a warp keeps 2 KB in flight. Chunk c of a row starting at
+// element s covers quads (s >> 2) + 32c ..; the few elements of the first and
+// last quad outside the row are replaced by the probe's sentinel. The chunks
+// come from a Cursor (rows held by the lanes, or a CTA's shared row table),
+// four at a time; one batch may span several rows.
+constexpr uint32_t kLongRow = 96;  // rows at least this long are read in quad chunks
+constexpr int kQU = 4;             // chunks per batch
 
-template <int ALGO, unsigned F, class Probe>
-__device__ __forceinline__ void stream_blocks(const ListParams& P, uint32_t seed, const uint32_t* rp, uint32_t len,
-                                              uint32_t kb, uint32_t ke, uint32_t x, const Probe& probe,
-                                              Sink<ALGO, F>& sink, unsigned& hits) {
-    constexpr int U = TRIGPU_STREAM_U;
+struct Chunk {
+    uint64_t qb;  // first quad (global quad index into out_adj)
+    int32_t r0;   // row-relative element index of lane 0's first element (-3 .. )
+    uint32_t len; // row length
+    uint32_t x;   // row owner (sinks)
+    bool valid;
+};
+
+__device__ __forceinline__ uint32_t row_chunks(uint64_t ro, uint32_t len) {
+    return len ? (static_cast<uint32_t>(ro & 3u) + len + 127u) >> 7 : 0u;
+}
+
+template <int ALGO, unsigned F, class Probe, class Cursor>
+__device__ __forceinline__ void stream_quads(const ListParams& P, uint32_t seed, Cursor& cur, const Probe& probe,
+                                             Sink<ALGO, F>& sink, unsigned& hits) {
     const unsigned lane = lane_id();
-    const uint32_t* p = rp + 32u * kb + lane;
-    uint32_t pos = 32u * kb + lane;
-    for (uint32_t k = kb; k < ke; k += U) {
-        const uint32_t* a[U];
-        uint32_t y[U];
-        bool ok[U], h[U];
+    const uint4* const quads = reinterpret_cast<const uint4*>(P.out_adj);
+    const uint32_t sent = probe.sentinel();
+    // chunks per batch: 4 (2 KB in flight per warp); 2 for the buffered sinks,
+    // whose batch / drain code would otherwise spill
+    constexpr int QU = Sink<ALGO, F>::kBuffered ? 2 : kQU;
+    while (cur.more()) {
+        Chunk ch[QU];
+        cur.next(ch);
+        const uint4* a[QU];
+        bool pr[QU];
+        uint4 y[QU];
+        int32_t r[QU];
 #pragma unroll
-        for (int i = 0; i < U; ++i) {
-            ok[i] = k + i < ke && pos + 32u * i < len;
-            a[i] = ok[i] ? p + 32 * i : rp;
+        for (int i = 0; i < QU; ++i) {
+            r[i] = ch[i].r0 + 4 * static_cast<int32_t>(lane);
+            pr[i] = ch[i].valid && r[i] < static_cast<int32_t>(ch[i].len);
+            a[i] = quads + ch[i].qb + lane;
+            y[i] = make_uint4(sent, sent, sent, sent);
         }
-        ldg_batch(a, y);
-        probe_batch(probe, y, ok, h);
+        ldgq(a, pr, y);
+#pragma unroll
+        for (int i = 0; i < QU; ++i) {
+            // partial first / last quad of a row: blank the elements outside it
+            if (pr[i] && (r[i] < 0 || static_cast<uint32_t>(r[i] + 4) > ch[i].len)) {
+                if (static_cast<uint32_t>(r[i]) >= ch[i].len) y[i].x = sent;
+                if (static_cast<uint32_t>(r[i] + 1) >= ch[i].len) y[i].y = sent;
+                if (static_cast<uint32_t>(r[i] + 2) >= ch[i].len) y[i].z = sent;
+                if (static_cast<uint32_t>(r[i] + 3) >= ch[i].len) y[i].w = sent;
+            }
+        }
+        uint32_t hb[QU];
         bool any = false;
 #pragma unroll
-        for (int i = 0; i < U; ++i) {
-            hits += h[i];
-            any |= h[i];
+        for (int i = 0; i < QU; ++i) {
+            hb[i] = probe.bit(y[i].x) | (probe.bit(y[i].y) << 1) | (probe.bit(y[i].z) << 2) | (probe.bit(y[i].w) << 3);
+            if constexpr (Probe::low)
+                any |= probe.below(y[i].x) | probe.below(y[i].y) | probe.below(y[i].z) | probe.below(y[i].w);
         }
-        if constexpr (F != 0u) {
+        if constexpr (Probe::low) {
+            // elements below the window: region-B candidates, verified here
             if (__any_sync(FULL, any)) {
 #pragma unroll
-                for (int i = 0; i < U; ++i) {
-                    sink.batch(h[i], x, y[i]);
-                    if (i % 2 == 1) sink.drain(P, seed);
+                for (int i = 0; i < QU; ++i) {
+                    const uint32_t e[4] = {y[i].x, y[i].y, y[i].z, y[i].w};
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const bool c = probe.below(e[k]) && probe.cand(e[k]);
+                        if (__any_sync(FULL, c))
+                            if (probe.verify(e[k], c)) hb[i] |= 1u << k;
+                    }
                 }
             }
         }
-        p += 32 * U;
-        pos += 32 * U;
+        uint32_t hm = 0;
+#pragma unroll
+        for (int i = 0; i < QU; ++i) hm |= hb[i] << (4 * i);
+        hits += __popc(hm);
+        if constexpr (Sink<ALGO, F>::kBuffered) {
+            if (__any_sync(FULL, hm != 0)) {
+#pragma unroll
+                for (int i = 0; i < QU; ++i) {
+                    if (__any_sync(FULL, hb[i] != 0)) {
+                        sink.batch(hb[i] & 1u, ch[i].x, y[i].x);
+                        sink.batch(hb[i] & 2u, ch[i].x, y[i].y);
+                        sink.drain(P, seed);
+                        sink.batch(hb[i] & 4u, ch[i].x, y[i].z);
+                        sink.batch(hb[i] & 8u, ch[i].x, y[i].w);
+                        sink.drain(P, seed);
+                    }
+                }
+            }
+        } else if constexpr (Sink<ALGO, F>::kFastSum) {
+            // per chunk: sum over its hits y of h(y), then one multiply by
+            // h(s) h(x). Straight-line predicated gathers (hub ranks: L1/L2
+            // hits), all in flight before the first use.
+            if (__any_sync(FULL, hm != 0)) {
+                unsigned long long sy[QU];
+#pragma unroll
+                for (int i = 0; i < QU; ++i) {
+                    const unsigned long long a0 = (hb[i] & 1u) ? __ldg(P.hv + y[i].x) : 0ull;
+                    const unsigned long long a1 = (hb[i] & 2u) ? __ldg(P.hv + y[i].y) : 0ull;
+                    const unsigned long long a2 = (hb[i] & 4u) ? __ldg(P.hv + y[i].z) : 0ull;
+                    const unsigned long long a3 = (hb[i] & 8u) ? __ldg(P.hv + y[i].w) : 0ull;
+                    sy[i] = (a0 + a1) + (a2 + a3);
+                }
+#pragma unroll
+                for (int i = 0; i < QU; ++i)
+                    if (hb[i]) sink.sum += sy[i] * (sink.hs * __ldg(P.hv + ch[i].x));
+            }
+        }
     }
 }
 
+// Rows held by the lanes (lane j: row of x_j at ro, rl elements); the cursor
+// visits the rows selected by `mask` in lane order, chunk by chunk. Four
+// chunks of one row are handed out at once when the row has them left.
+struct LaneRowCursor {
+    uint64_t ro;
+    uint32_t rl, xl;  // this lane's row
+    unsigned left;    // rows not started yet
+    uint64_t q0;      // current row (uniform): first quad
+    int32_t h;        // s & 3
+    uint32_t len, x, c, nch;
+    bool on;
+    __device__ __forceinline__ LaneRowCursor(uint64_t ro_, uint32_t rl_, uint32_t x_, unsigned mask)
+        : ro(ro_), rl(rl_), xl(x_), left(mask), q0(0), h(0), len(0), x(0), c(0), nch(0), on(false) {
+        advance();
+    }
+    __device__ __forceinline__ void advance() {
+        on = left != 0;
+        if (!on) return;
+        const int j = __ffs(left) - 1;
+        left &= left - 1;
+        const uint64_t s = shfl64(ro, j);
+        len = __shfl_sync(FULL, rl, j);
+        x = __shfl_sync(FULL, xl, j);
+        q0 = s >> 2;
+        h = static_cast<int32_t>(s & 3u);
+        c = 0;
+        nch = (static_cast<uint32_t>(h) + len + 127u) >> 7;
+    }
+    __device__ __forceinline__ bool more() const { return on; }
+    __device__ __forceinline__ Chunk at(uint32_t cc) const {
+        return Chunk{q0 + 32u * cc, static_cast<int32_t>(128u * cc) - h, len, x, true};
+    }
+    template <int N>
+    __device__ __forceinline__ void next(Chunk (&ch)[N]) {
+        if (c + N <= nch) {  // fast path: N chunks of the current row
+#pragma unroll
+            for (int i = 0; i < N; ++i) ch[i] = at(c + i);
+            c += N;
+            if (c == nch) advance();
+            return;
+        }
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            if (on) {
+                ch[i] = at(c);
+                if (++c == nch) advance();
+            } else {
+                ch[i] = Chunk{0, 0, 0, 0, false};
+            }
+        }
+    }
+};
+
+// A warp's contiguous range [g, ge) of a CTA seed's chunks (shared row table
+// {ro lo, ro hi, len, first chunk}), walked forward row by row.
+struct CtaRowCursor {
+    unsigned rows;
+    const uint32_t* xs;  // the seed's set row: x of row i
+    uint32_t g, ge, i, rf, rend, x, len;
+    uint64_t q0;
+    int32_t h;
+    __device__ __forceinline__ CtaRowCursor(unsigned rows_, const uint32_t* xs_, uint32_t d, uint32_t gb, uint32_t ge_)
+        : rows(rows_), xs(xs_), g(gb), ge(ge_) {
+        uint32_t lo = 0, hi = d - 1;
+        while (lo < hi) {  // last row i with first_chunk(i) <= gb
+            const uint32_t mid = (lo + hi + 1) >> 1;
+            if (lds32(rows + 16u * mid + 12u) <= gb) lo = mid;
+            else hi = mid - 1;
+        }
+        i = lo;
+        load();
+    }
+    __device__ __forceinline__ void load() {
+        const uint4 r = lds128(rows + 16u * i);
+        const uint64_t ro = (static_cast<uint64_t>(r.y) << 32) | r.x;
+        len = r.z;
+        rf = r.w;
+        rend = rf + row_chunks(ro, len);
+        q0 = ro >> 2;
+        h = static_cast<int32_t>(r.x & 3u);
+        x = __ldg(xs + i);
+    }
+    __device__ __forceinline__ bool more() const { return g < ge; }
+    __device__ __forceinline__ Chunk at(uint32_t gg) const {
+        const uint32_t cc = gg - rf;
+        return Chunk{q0 + 32u * cc, static_cast<int32_t>(128u * cc) - h, len, x, true};
+    }
+    template <int N>
+    __device__ __forceinline__ void next(Chunk (&ch)[N]) {
+        if (g + N <= rend && g + N <= ge) {  // fast path: N chunks of the current row
+#pragma unroll
+            for (int k = 0; k < N; ++k) ch[k] = at(g + k);
+            g += N;
+            return;
+        }
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+            if (g < ge) {
+                while (g >= rend) {
+                    ++i;
+                    load();
+                }
+                ch[k] = at(g);
+                ++g;
+            } else {
+                ch[k] = Chunk{0, 0, 0, 0, false};
+            }
+        }
+    }
+};
+
 // Walk the out-rows of up to 32 x's (x valid on lanes with xvalid), probing
-// every element y against the seed's set. Two phases:
-//   1. rows of >= 32 elements, as 128-byte-ALIGNED blocks of 32 elements
-//      (partial first / last block predicated), flattened over all blocks of
-//      all such rows: block g belongs to row j = #rows whose blocks end at or
-//      before g (one vote); the row's block offset and edge lanes come from a
-//      per-warp shared-memory table read with a broadcast LDS; lane l reads
-//      element l of the block (one fully coalesced 128 B line). Software-
-//      pipelined: the next four blocks' loads are issued before the current
-//      four are probed (up to eight loads in flight per lane);
-//   2. rows of < 32 elements as ONE flattened stream (lane f of a window
-//      reads element f of the concatenated rows; the owning row of each lane
-//      comes from an OR-reduction of the row starts), so short rows do not
-//      idle lanes.
+// every element y against the seed's set:
+//   1. rows of >= kLongRow elements as quad chunks (stream_quads);
+//   2. shorter rows as ONE flattened stream (lane f of a window reads
+//      element f of the concatenated rows; the owning row of each lane comes
+//      from an OR-reduction of the row starts), so short rows do not idle lanes.
 template <int ALGO, unsigned F, class Probe>
 __device__ __forceinline__ void scan_rows(const ListParams& P, uint32_t seed, uint32_t x, bool xvalid,
                                           const Probe& probe, Sink<ALGO, F>& sink) {
@@ -259,17 +564,13 @@ __device__ __forceinline__ void scan_rows(const ListParams& P, uint32_t seed, ui
         rl = static_cast<uint32_t>(P.out_off[x + 1] - ro);
     }
     unsigned hits = 0;
-    // ---- phase 1: rows of >= 32 elements, one at a time, whole warp per row
-    unsigned longm = __ballot_sync(FULL, rl >= 32u);
-    while (longm) {
-        const int j = __ffs(longm) - 1;
-        longm &= longm - 1;
-        const uint32_t len = __shfl_sync(FULL, rl, j);
-        const uint32_t* rp = P.out_adj + shfl64(ro, j);
-        stream_blocks<ALGO, F>(P, seed, rp, len, 0, (len + 31u) >> 5, __shfl_sync(FULL, x, j), probe, sink, hits);
+    // ---- phase 1: long rows, quad chunks
+    {
+        LaneRowCursor cur(ro, rl, x, __ballot_sync(FULL, rl >= kLongRow));
+        stream_quads<ALGO, F>(P, seed, cur, probe, sink, hits);
     }
-    if (rl >= 32u) rl = 0;
-    // ---- phase 2: tails
+    if (rl >= kLongRow) rl = 0;
+    // ---- phase 2: short rows
     const unsigned ne = __ballot_sync(FULL, rl != 0);
     if (!ne) {
         sink.cnt += hits;
@@ -308,13 +609,19 @@ __device__ __forceinline__ void scan_rows(const ListParams& P, uint32_t seed, ui
         const uint64_t rbB = shfl64(rbase, jB);
         const uint32_t yA = actA ? __ldg(P.out_adj + rbA + fA) : kNone;
         const uint32_t yB = actB ? __ldg(P.out_adj + rbB + fB) : kNone;
-        const bool hitA = probe(yA, actA);
-        const bool hitB = probe(yB, actB);
+        const bool hitA = probe_one(probe, yA, actA);
+        const bool hitB = probe_one(probe, yB, actB);
         hits += (unsigned)hitA + (unsigned)hitB;
-        if constexpr (F != 0u) {
-            sink.batch(hitA, __shfl_sync(FULL, cx, jA), yA);
-            sink.batch(hitB, __shfl_sync(FULL, cx, jB), yB);
-            sink.drain(P, seed);
+        if constexpr (Sink<ALGO, F>::kBuffered || Sink<ALGO, F>::kFastSum) {
+            const uint32_t xA = __shfl_sync(FULL, cx, jA), xB = __shfl_sync(FULL, cx, jB);
+            if constexpr (Sink<ALGO, F>::kBuffered) {
+                sink.batch(hitA, xA, yA);
+                sink.batch(hitB, xB, yB);
+                sink.drain(P, seed);
+            } else {
+                sink.direct(P, hitA, xA, yA);
+                sink.direct(P, hitB, xB, yB);
+            }
         }
     }
     sink.cnt += hits;
@@ -323,7 +630,7 @@ __device__ __forceinline__ void scan_rows(const ListParams& P, uint32_t seed, ui
 // Chunks of 32 x's: set elements c, c + stride, ... below xe of the seed row at so.
 template <int ALGO, unsigned F, class Probe>
 __device__ __forceinline__ void scan_x_range(const ListParams& P, uint32_t seed, uint64_t so, uint32_t cb,
-                                             uint32_t xe, uint32_t stride, Probe probe, Sink<ALGO, F>& sink) {
+                                             uint32_t xe, uint32_t stride, const Probe& probe, Sink<ALGO, F>& sink) {
     const unsigned lane = lane_id();
     for (uint32_t c = cb; c < xe; c += stride) {
         const bool xv = c + lane < xe;
@@ -332,476 +639,210 @@ __device__ __forceinline__ void scan_x_range(const ListParams& P, uint32_t seed,
     }
 }
 
-// ---- probes --------------------------------------------------------------
-
-struct RegProbe {  // S sorted ascending, one element per lane, padded with kNone
-    uint32_t s;
-    __device__ __forceinline__ bool operator()(uint32_t y, bool act) const {
-        int pos = 0;
-#pragma unroll
-        for (int step = 16; step; step >>= 1) {
-            const uint32_t v = __shfl_sync(FULL, s, pos + step - 1);
-            if (v < y) pos += step;
-        }
-        const uint32_t v = __shfl_sync(FULL, s, pos & 31);
-        return act && pos < 32 && v == y;
-    }
-};
-
-// Probe structure of classes H and C: a direct bitmap over the top window
-// [wbase, n) of the rank space plus a bucketised hash table for the rest.
-//
-// Under degree ordering on power-law graphs the scanned rows N+(x) are made
-// of hubs, i.e. the top ranks: on R-MAT, 90 % of all probes hit the top
-// 0.2 % of ranks (scale 22). A sorted row's 32-element block therefore falls
-// in a handful of bitmap words, so the window probe is one LDS.32 that the
-// lanes of a warp mostly share (broadcast, no bank conflicts) and it is exact.
-// Other probes go to the hash table: nb (power of two) buckets of four u32
-// slots, one 16-byte LDS.128 per probe, slots filled in order (slot 3 used
-// <=> bucket full), overflow keys in a small stash scanned only for full
-// buckets. If even the stash overflows the seed falls back to a binary
-// search of its sorted row in global memory, so the result stays exact.
-constexpr uint32_t kStash = 32;
-
-struct BucketTable {
-    uint32_t* slots;      // 4 * nb u32, shared memory
-    uint32_t* stash;      // kStash u32, shared memory
-    unsigned* nstash;     // shared counter (> kStash: overflowed)
-    uint32_t* win;        // window bitmap, shared memory
-    uint32_t wbase;       // first rank of the window
-};
-
-__device__ __forceinline__ uint32_t bucket_shift(uint32_t d, uint32_t max_bits) {
-    // nb = smallest power of two >= 2d (<= 1/2 key per slot-quad on average), >= 16
-    uint32_t bits = 32 - __clz(max(2u * d - 1u, 15u));
-    bits = bits > max_bits ? max_bits : bits;
-    return 32 - bits;
-}
-
-__device__ __forceinline__ void bucket_insert(const BucketTable& T, uint32_t shift, uint32_t key) {
-#ifdef TRIGPU_HUB_WINDOW
-    if (key >= T.wbase) {
-        const uint32_t o = key - T.wbase;
-        atomicOr(T.win + (o >> 5), 1u << (o & 31));
-        return;
-    }
-#endif
-    uint32_t* b = T.slots + 4u * ((key * 0x9E3779B1u) >> shift);
-#pragma unroll
-    for (int s = 0; s < 4; ++s)
-        if (atomicCAS(&b[s], kNone, key) == kNone) return;
-    const unsigned i = atomicAdd(T.nstash, 1u);
-    if (i < kStash) T.stash[i] = key;
-}
-
-__device__ __forceinline__ void bucket_clear(const BucketTable& T, uint32_t shift, uint32_t key) {
-#ifdef TRIGPU_HUB_WINDOW
-    if (key >= T.wbase) {
-        T.win[(key - T.wbase) >> 5] = 0u;
-        return;
-    }
-#endif
-    uint4* b = reinterpret_cast<uint4*>(T.slots) + ((key * 0x9E3779B1u) >> shift);
-    *b = make_uint4(kNone, kNone, kNone, kNone);
-}
-
-template <bool kStashed>
-struct BucketProbe {
-    unsigned win;     // shared address of the window bitmap
-    uint32_t wbase;
-    unsigned slots;   // shared address of the bucket array
-    unsigned stash;   // shared address of the stash
-    uint32_t shift;
-    uint32_t nstash;  // kStashed == false <=> nstash == 0 (the common case)
-    __device__ __forceinline__ bool operator()(uint32_t y, bool act) const {
-#ifdef TRIGPU_HUB_WINDOW
-        if (!act) return false;
-        if (y >= wbase) {
-            const uint32_t o = y - wbase;
-            return (lds32(win + 4u * (o >> 5)) >> (o & 31)) & 1u;
-        }
-#endif
-        const uint4 v = lds128(slots + 16u * ((y * 0x9E3779B1u) >> shift));
-        bool hit = (v.x == y) | (v.y == y) | (v.z == y) | (v.w == y);
-        if constexpr (kStashed) {
-            if (act && !hit && v.w != kNone)
-                for (uint32_t i = 0; i < nstash; ++i) hit |= lds32(stash + 4u * i) == y;
-        }
-        return act && hit;
-    }
-    // N probes at once: window words as predicated LDS.32 (no branches), the
-    // hash path only if some lane of the warp has a below-window element.
-    template <int N>
-    __device__ __forceinline__ void batch(const uint32_t (&y)[N], const bool (&ok)[N], bool (&h)[N]) const {
-#ifndef TRIGPU_HUB_WINDOW
-#pragma unroll
-        for (int k = 0; k < N; ++k) h[k] = (*this)(y[k], ok[k]);
-        return;
-#endif
-        bool need = false;
-#pragma unroll
-        for (int k = 0; k < N; ++k) {
-            const bool inw = ok[k] && y[k] >= wbase;
-            const uint32_t o = y[k] - wbase;
-            const uint32_t w = lds32_if(win + 4u * (o >> 5), inw);
-            h[k] = (w >> (o & 31)) & 1u;
-            need |= ok[k] && !inw;
-        }
-        if (__any_sync(FULL, need)) {
-#pragma unroll
-            for (int k = 0; k < N; ++k)
-                if (ok[k] && y[k] < wbase) h[k] = (*this)(y[k], true);
-        }
-    }
-};
-
-// Default batched probe: N scalar probes.
-template <class Probe, int N>
-__device__ __forceinline__ void probe_batch(const Probe& p, const uint32_t (&y)[N], const bool (&ok)[N],
-                                            bool (&h)[N]) {
-#pragma unroll
-    for (int k = 0; k < N; ++k) h[k] = p(y[k], ok[k]);
-}
-template <bool S, int N>
-__device__ __forceinline__ void probe_batch(const BucketProbe<S>& p, const uint32_t (&y)[N], const bool (&ok)[N],
-                                            bool (&h)[N]) {
-    p.batch(y, ok, h);
-}
-
-// Exact fallback: binary search of the seed's sorted set row (global).
-struct SearchProbe {
-    const uint32_t* row;
-    uint32_t d;
-    __device__ __forceinline__ bool operator()(uint32_t y, bool act) const {
-        if (!act) return false;
-        uint32_t lo = 0, hi = d;
-        while (lo < hi) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (__ldg(row + mid) < y) lo = mid + 1;
-            else hi = mid;
-        }
-        return lo < d && __ldg(row + lo) == y;
-    }
-};
-
-// Timing-only probe (TRIGPU_VARIANT=2): touches every loaded element, never
-// hits. Measures the row-streaming limit of a kernel without the probe cost.
-struct NullProbe {
-    __device__ __forceinline__ bool operator()(uint32_t y, bool act) const { return act && y == 0xFFFFFFFEu; }
-};
-
-// Dispatch on the table state of the current seed (uniform per unit).
-template <class Body>
-__device__ __forceinline__ void dispatch_probe(const BucketTable& T, uint32_t shift, unsigned ns,
-                                               const uint32_t* row, uint32_t d, int variant, Body&& body) {
+// Run body(probe) with the seed's bitmap: window only, or window + region B.
+template <class V, class Body>
+__device__ __forceinline__ void with_win_probe(const ListParams& P, unsigned bma, unsigned bmb, const WinGeom& g,
+                                               const V& ver, Body&& body) {
 #ifdef TRIGPU_EXPERIMENTS
-    if (variant == 2) {
+    if (P.variant == 2) {
         body(NullProbe{});
         return;
     }
 #endif
-    if (ns == 0)
-        body(BucketProbe<false>{smem_addr(T.win), T.wbase, smem_addr(T.slots), 0, shift, 0});
-    else if (ns <= kStash)
-        body(BucketProbe<true>{smem_addr(T.win), T.wbase, smem_addr(T.slots), smem_addr(T.stash), shift, ns});
-    else
-        body(SearchProbe{row, d});
+    if (!g.low) body(WinProbe<false, V>{bma, bmb, g.wb, g.la, g.maskb, ver});
+    else body(WinProbe<true, V>{bma, bmb, g.wb, g.la, g.maskb, ver});
 }
-
-struct BitmapProbe {
-    const uint32_t* bm;
-    __device__ __forceinline__ bool operator()(uint32_t y, bool act) const {
-        if (!act) return false;
-        return (__ldcg(bm + (y >> 5)) >> (y & 31)) & 1u;
-    }
-};
 
 // ---- per-warp scratch in dynamic shared memory ------------------------------
-// [warps x kMetaBytes row tables][warps x kHitBuf uint2 hit buffers, F != 0]
-// followed by the kernel's probe tables.
-#ifndef TRIGPU_RING
-#define TRIGPU_RING 0
-#endif
-constexpr uint32_t kRing = 8;  // blocks in flight per warp (power of two)
-constexpr size_t kRingBytes = TRIGPU_RING ? kRing * 128 : 0;
-
+// [warps x kHitBuf uint2 hit buffers (buffered sinks only)] followed by the
+// kernel's bitmaps.
 template <unsigned F>
 __host__ __device__ constexpr size_t warp_scratch_bytes(int warps) {
-    return static_cast<size_t>(warps) * ((F ? kHitBuf * 8 : 0) + kRingBytes);
+    return (F & (F_VCOUNT | F_LIST)) ? static_cast<size_t>(warps) * kHitBuf * 8 : 0;
 }
 
 template <int ALGO, unsigned F>
-__device__ __forceinline__ void attach_scratch(Sink<ALGO, F>& sink, unsigned char* base, int warps) {
-    const unsigned w = threadIdx.x >> 5;
-    if constexpr (F != 0u) sink.buf = smem_addr(base + w * kHitBuf * 8);
-    sink.ring = smem_addr(base + warps * (F ? kHitBuf * 8 : 0) + w * kRingBytes);
+__device__ __forceinline__ void attach_scratch(Sink<ALGO, F>& sink, unsigned char* base) {
+    sink.buf = smem_addr(base + (threadIdx.x >> 5) * kHitBuf * 8);
 }
 
-// ---- class R: |S| <= 32, warp per seed, S in registers -------------------
+#ifndef TRIGPU_WARP_MINB
+#define TRIGPU_WARP_MINB 4
+#endif
+
+// ---- class R: |S| <= 32, warp per seed --------------------------------------
 constexpr int kRWarps = 8;
+constexpr uint32_t kRBitsA = 13, kRBitsB = 11;  // 1 KB window + 256 B region B per warp
+constexpr size_t kRBmBytes = win_bytes(kRBitsA, kRBitsB);
 
 template <int ALGO, unsigned F>
-__global__ void __launch_bounds__(kRWarps * 32) k_list_reg(ListParams P) {
+__global__ void __launch_bounds__(kRWarps * 32, TRIGPU_WARP_MINB) k_list_reg(ListParams P) {
     extern __shared__ __align__(16) unsigned char dsm[];
-    const unsigned lane = lane_id();
+    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+    uint32_t* bma = reinterpret_cast<uint32_t*>(dsm + warp_scratch_bytes<F>(kRWarps) + warp * kRBmBytes);
+    uint32_t* bmb = bma + ((1u << kRBitsA) / 32 + 4);
+    for (uint32_t i = lane; i < kRBmBytes / 4; i += 32) bma[i] = 0u;
+    __syncwarp();
     Sink<ALGO, F> sink;
-    attach_scratch(sink, dsm, kRWarps);
+    attach_scratch(sink, dsm);
     for (;;) {
         unsigned i = 0;
         if (lane == 0) i = atomicAdd(P.queue, 1u);
         i = __shfl_sync(FULL, i, 0);
         if (i >= P.nseeds) break;
         const uint32_t seed = P.seeds[i];
+        sink.begin_unit(P, seed);
         const uint64_t so = P.set_off[seed];
         const uint32_t d = static_cast<uint32_t>(P.set_off[seed + 1] - so);
         const uint32_t s = lane < d ? __ldg(P.set_adj + so + lane) : kNone;
-#ifdef TRIGPU_EXPERIMENTS
-        if (P.variant == 2) {
-            scan_rows<ALGO, F>(P, seed, s, lane < d, NullProbe{}, sink);
-            sink.end_unit(P, seed);
-            continue;
-        }
-#endif
-        scan_rows<ALGO, F>(P, seed, s, lane < d, RegProbe{s}, sink);
+        const WinGeom g = win_geom(kRBitsA, kRBitsB, P.bm_shrink, __shfl_sync(FULL, s, 0), __shfl_sync(FULL, s, d - 1));
+        if (lane < d) win_set(bma, bmb, g, s);
+        __syncwarp();
+        with_win_probe(P, smem_addr(bma), smem_addr(bmb), g, RegVerify{s}, [&](const auto& probe) {
+            scan_rows<ALGO, F>(P, seed, s, lane < d, probe, sink);
+        });
         sink.end_unit(P, seed);
+        __syncwarp();
+        if (lane < d) win_clear(bma, bmb, g, s);
+        __syncwarp();
     }
     sink.flush(P);
 }
 
-// ---- class H: 32 < |S| <= 256, warp per seed, per-warp probe table ------
+// ---- class H: 32 < |S| <= 256, warp per seed --------------------------------
 constexpr int kHWarps = 8;
-constexpr uint32_t kHMaxBits = 8;     // 256 buckets = 4 KB per warp
-constexpr uint32_t kHWinBits = 13;    // 8192-rank window = 1 KB per warp
-constexpr size_t kHTableBytes = (16u << kHMaxBits) + (1u << kHWinBits) / 8 + kStash * 4 + 16;
-
-// wbase for a window of 2^win_bits top ranks; win_bits == 0 disables it.
-__device__ __forceinline__ uint32_t window_base(uint32_t n, uint32_t win_bits) {
-    if (win_bits == 0) return 0xFFFFFFFFu;
-    return n > (1u << win_bits) ? n - (1u << win_bits) : 0u;
-}
+constexpr uint32_t kHBitsA = 15, kHBitsB = 13;  // 4 KB window + 1 KB region B per warp
+constexpr size_t kHBmBytes = win_bytes(kHBitsA, kHBitsB);
 
 template <int ALGO, unsigned F>
-__global__ void __launch_bounds__(kHWarps * 32) k_list_hash_warp(ListParams P) {
+__global__ void __launch_bounds__(kHWarps * 32, TRIGPU_WARP_MINB) k_list_warp(ListParams P) {
     extern __shared__ __align__(16) unsigned char dsm[];
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
-    unsigned char* tbase = dsm + warp_scratch_bytes<F>(kHWarps) + warp * kHTableBytes;
-    constexpr uint32_t kSlotBytes = 16u << kHMaxBits, kWinBytes = (1u << kHWinBits) / 8;
-    BucketTable T{reinterpret_cast<uint32_t*>(tbase), reinterpret_cast<uint32_t*>(tbase + kSlotBytes + kWinBytes),
-                  reinterpret_cast<unsigned*>(tbase + kSlotBytes + kWinBytes + kStash * 4),
-                  reinterpret_cast<uint32_t*>(tbase + kSlotBytes),
-                  window_base(P.n, min(P.win_bits, kHWinBits))};
-    for (uint32_t i = lane; i < (4u << kHMaxBits); i += 32) T.slots[i] = kNone;
-    for (uint32_t i = lane; i < kWinBytes / 4; i += 32) T.win[i] = 0u;
-    if (lane == 0) *T.nstash = 0;
+    uint32_t* bma = reinterpret_cast<uint32_t*>(dsm + warp_scratch_bytes<F>(kHWarps) + warp * kHBmBytes);
+    uint32_t* bmb = bma + ((1u << kHBitsA) / 32 + 4);
+    for (uint32_t i = lane; i < kHBmBytes / 4; i += 32) bma[i] = 0u;
     __syncwarp();
     Sink<ALGO, F> sink;
-    attach_scratch(sink, dsm, kHWarps);
+    attach_scratch(sink, dsm);
     for (;;) {
         unsigned i = 0;
         if (lane == 0) i = atomicAdd(P.queue, 1u);
         i = __shfl_sync(FULL, i, 0);
         if (i >= P.nseeds) break;
         const uint32_t seed = P.seeds[i];
+        sink.begin_unit(P, seed);
         const uint64_t so = P.set_off[seed];
         const uint32_t d = static_cast<uint32_t>(P.set_off[seed + 1] - so);
-        const uint32_t shift = bucket_shift(d, kHMaxBits);
-        for (uint32_t k = lane; k < d; k += 32) bucket_insert(T, shift, __ldg(P.set_adj + so + k));
+        const uint32_t* row = P.set_adj + so;
+        const WinGeom g = win_geom(kHBitsA, kHBitsB, P.bm_shrink, __ldg(row), __ldg(row + d - 1));
+        for (uint32_t k = lane; k < d; k += 32) win_set(bma, bmb, g, __ldg(row + k));
         __syncwarp();
-        dispatch_probe(T, shift, *T.nstash, P.set_adj + so, d, P.variant, [&](const auto& probe) {
+        with_win_probe(P, smem_addr(bma), smem_addr(bmb), g, RowVerify{row, d}, [&](const auto& probe) {
             scan_x_range<ALGO, F>(P, seed, so, 0, d, 32, probe, sink);
         });
         sink.end_unit(P, seed);
         __syncwarp();
-        for (uint32_t k = lane; k < d; k += 32) bucket_clear(T, shift, __ldg(P.set_adj + so + k));
-        if (lane == 0) *T.nstash = 0;
+        for (uint32_t k = lane; k < d; k += 32) win_clear(bma, bmb, g, __ldg(row + k));
         __syncwarp();
     }
     sink.flush(P);
 }
 
-// ---- class C: 256 < |S| <= 4096, CTA per seed, bucket table -------------
-// All 32 warps of the CTA share the seed's table. The seed's rows are cut
-// into 32-element blocks (block prefix over the set in shared memory) and
-// warps pull batches of kCBatch blocks from a shared counter, so the CTA
-// barrier at the end of a seed waits for at most one batch per warp.
-// Two sizes: C1 (256 < |S| <= 1024) runs 8-warp CTAs, several per SM, so one
-// CTA's seed barrier is hidden by the others; C2 (1024 < |S| <= 4096) needs
-// the 64 KB table and runs one 32-warp CTA per SM.
-template <int THREADS, uint32_t MAXBITS, uint32_t MAXD, int MINB>
+// ---- class C: 256 < |S| <= 4096, CTA per seed ----------------------------------
+// All warps of the CTA share the seed's bitmap. The seed's rows are cut into
+// chunks (chunk prefix over the set in a shared row table) and split equally
+// across the warps, so the CTA barrier at the end of a seed waits for
+// balanced work. Two sizes: C1 (256 < |S| <= 1024) runs 8-warp CTAs, several
+// per SM, so one CTA's seed barrier is hidden by the others; C2 (1024 < |S| <=
+// 4096) runs one 32-warp CTA per SM.
+template <int THREADS, uint32_t BITS_A, uint32_t BITS_B, uint32_t MAXD, int MINB>
 struct CtaCfg {
     static constexpr int kThreads = THREADS;
     static constexpr int kWarps = THREADS / 32;
-    static constexpr uint32_t kMaxBits = MAXBITS;  // 2^MAXBITS buckets
+    static constexpr uint32_t kBitsA = BITS_A;  // window of 2^BITS_A ranks
+    static constexpr uint32_t kBitsB = BITS_B;  // region B of 2^BITS_B bits
     static constexpr uint32_t kMaxD = MAXD;
     static constexpr int kMinBlocks = MINB;
 };
-using CfgC1 = CtaCfg<256, 11, 1024, 4>;
-using CfgC2 = CtaCfg<1024, 12, 4096, 1>;
-constexpr uint32_t kCBatch = 4;
-constexpr uint32_t kCWinBits = 18;  // 262144-rank window = 32 KB
-#ifdef TRIGPU_HUB_WINDOW
-constexpr uint32_t kCWinBytes = (1u << kCWinBits) / 8;
-#else
-constexpr uint32_t kCWinBytes = 16;
-#endif
+using CfgC1 = CtaCfg<256, 18, 14, 1024, 3>;
+using CfgC2 = CtaCfg<1024, 19, 15, 4096, 1>;
 template <class CFG>
-constexpr size_t cta_table_bytes() { return (16u << CFG::kMaxBits) + kCWinBytes + kStash * 4 + 16; }
+constexpr size_t cta_bitmap_bytes() { return win_bytes(CFG::kBitsA, CFG::kBitsB); }
 template <class CFG>
-constexpr size_t cta_row_bytes() { return CFG::kMaxD * 16; }  // uint4 {ro lo, ro hi, len, first block}
-
-template <int ALGO, unsigned F, class CFG, class Probe>
-__device__ __forceinline__ void cta_blocks(const ListParams& P, uint32_t seed, uint64_t so, uint32_t d,
-                                           unsigned rows, uint32_t nblocks, const Probe& probe,
-                                           Sink<ALGO, F>& sink) {
-    const unsigned warp = threadIdx.x >> 5;
-    // equal share of the seed's blocks per warp (equal work), contiguous so
-    // the owning rows are found once and then walked forward
-    const uint32_t gb = static_cast<uint32_t>((static_cast<uint64_t>(nblocks) * warp) / CFG::kWarps);
-    const uint32_t ge = static_cast<uint32_t>((static_cast<uint64_t>(nblocks) * (warp + 1)) / CFG::kWarps);
-    if (gb >= ge) return;
-    uint32_t lo = 0, hi = d - 1;
-    while (lo < hi) {  // last row i with first_block(i) <= gb
-        const uint32_t mid = (lo + hi + 1) >> 1;
-        if (lds32(rows + 16u * mid + 12u) <= gb) lo = mid;
-        else hi = mid - 1;
-    }
-    unsigned hits = 0;
-#if TRIGPU_RING
-    // kRing blocks in flight per warp through cp.async into a shared-memory
-    // ring (lane l copies and later reads only its own word of each slot),
-    // so the depth costs no registers. Two cursors walk the rows: one issues
-    // block g + kRing while the other consumes block g.
-    const unsigned ring = sink.ring;
-    const unsigned lane = lane_id();
-    uint32_t ii = lo, ci = lo;
-    uint4 ir = lds128(rows + 16u * lo), cr = ir;
-    uint32_t inext = lo + 1 < d ? lds32(rows + 16u * (lo + 1) + 12u) : 0xFFFFFFFFu, cnext = inext;
-    uint32_t gi = gb;
-    auto issue = [&](uint32_t slot) {
-        if (gi < ge) {
-            while (inext <= gi) {
-                ++ii;
-                ir = lds128(rows + 16u * ii);
-                inext = ii + 1 < d ? lds32(rows + 16u * (ii + 1) + 12u) : 0xFFFFFFFFu;
-            }
-            const uint32_t pos = 32u * (gi - ir.w) + lane;
-            if (pos < ir.z)
-                cp_async4(ring + 128u * slot + 4u * lane,
-                          P.out_adj + ((static_cast<uint64_t>(ir.y) << 32) | ir.x) + pos);
-        }
-        cp_async_commit();
-        ++gi;
-    };
-#pragma unroll
-    for (uint32_t s = 0; s < kRing; ++s) issue(s);
-    for (uint32_t g = gb; g < ge; ++g) {
-        cp_async_wait<kRing - 1>();
-        const uint32_t slot = (g - gb) & (kRing - 1);
-        while (cnext <= g) {
-            ++ci;
-            cr = lds128(rows + 16u * ci);
-            cnext = ci + 1 < d ? lds32(rows + 16u * (ci + 1) + 12u) : 0xFFFFFFFFu;
-        }
-        const bool ok = 32u * (g - cr.w) + lane < cr.z;
-        const uint32_t y = ok ? lds32(ring + 128u * slot + 4u * lane) : kNone;
-        const bool h = probe(y, ok);
-        hits += h;
-        if constexpr (F != 0u) {
-            if (__any_sync(FULL, h)) sink.batch(h, __ldg(P.set_adj + so + ci), y);
-            if (((g - gb) & 1u) == 1u) sink.drain(P, seed);
-        }
-        issue(slot);
-    }
-    cp_async_wait<0>();
-#else
-    for (uint32_t i = lo, g = gb; g < ge && i < d; ++i) {
-        const uint4 r = lds128(rows + 16u * i);  // {ro lo, ro hi, len, first block}
-        const uint32_t nb = (r.z + 31u) >> 5;
-        if (r.w + nb <= g) continue;  // empty row (or already covered)
-        const uint32_t kb = g - r.w, ke = min(ge - r.w, nb);
-        const uint32_t x = F ? __ldg(P.set_adj + so + i) : 0u;
-        stream_blocks<ALGO, F>(P, seed, P.out_adj + ((static_cast<uint64_t>(r.y) << 32) | r.x), r.z, kb, ke, x,
-                               probe, sink, hits);
-        g = r.w + ke;
-    }
-#endif
-    sink.cnt += hits;
-}
+constexpr size_t cta_row_bytes() { return CFG::kMaxD * 16; }  // uint4 {ro lo, ro hi, len, first chunk}
 
 template <int ALGO, unsigned F, class CFG>
-__global__ void __launch_bounds__(CFG::kThreads, CFG::kMinBlocks) k_list_hash_cta(ListParams P) {
+__global__ void __launch_bounds__(CFG::kThreads, CFG::kMinBlocks) k_list_cta(ListParams P) {
     constexpr int kCThreads = CFG::kThreads;
-    constexpr int kCWarps = CFG::kWarps;
-    constexpr uint32_t kCMaxBits = CFG::kMaxBits;
-    constexpr uint32_t kCMaxD = CFG::kMaxD;
-    constexpr size_t kCTableBytes = cta_table_bytes<CFG>();
+    constexpr uint32_t kWords = cta_bitmap_bytes<CFG>() / 4;
     extern __shared__ __align__(16) unsigned char dsm[];
-    __shared__ unsigned unit, next_block, total_blocks;
+    __shared__ unsigned unit, total_chunks;
     using BS = cub::BlockScan<uint32_t, kCThreads>;
     __shared__ typename BS::TempStorage scan_tmp;
-    unsigned char* tbase = dsm + warp_scratch_bytes<F>(kCWarps);
-    constexpr uint32_t kSlotBytes = 16u << kCMaxBits, kWinBytes = kCWinBytes;
-    BucketTable T{reinterpret_cast<uint32_t*>(tbase), reinterpret_cast<uint32_t*>(tbase + kSlotBytes + kWinBytes),
-                  reinterpret_cast<unsigned*>(tbase + kSlotBytes + kWinBytes + kStash * 4),
-                  reinterpret_cast<uint32_t*>(tbase + kSlotBytes),
-                  window_base(P.n, min(P.win_bits, kCWinBits))};
-    const unsigned rows = smem_addr(tbase + kCTableBytes);
-    for (uint32_t i = threadIdx.x; i < (4u << kCMaxBits); i += kCThreads) T.slots[i] = kNone;
-    for (uint32_t i = threadIdx.x; i < kWinBytes / 4; i += kCThreads) T.win[i] = 0u;
-    if (threadIdx.x == 0) *T.nstash = 0;
+    uint32_t* bma = reinterpret_cast<uint32_t*>(dsm + warp_scratch_bytes<F>(CFG::kWarps));
+    uint32_t* bmb = bma + ((1u << CFG::kBitsA) / 32 + 4);
+    const unsigned rows = smem_addr(dsm + warp_scratch_bytes<F>(CFG::kWarps) + cta_bitmap_bytes<CFG>());
+    for (uint32_t i = threadIdx.x; i < kWords; i += kCThreads) bma[i] = 0u;
     Sink<ALGO, F> sink;
-    attach_scratch(sink, dsm, kCWarps);
-    constexpr int PER = kCMaxD / kCThreads;  // set elements per thread
+    attach_scratch(sink, dsm);
+    constexpr int PER = CFG::kMaxD / kCThreads;  // set elements per thread
     for (;;) {
         __syncthreads();
-        if (threadIdx.x == 0) {
-            unit = atomicAdd(P.queue, 1u);
-            next_block = 0;
-        }
+        if (threadIdx.x == 0) unit = atomicAdd(P.queue, 1u);
         __syncthreads();
         const unsigned u = unit;
         if (u >= P.nseeds) break;
         const uint32_t seed = P.seeds[u];
+        sink.begin_unit(P, seed);
         const uint64_t so = P.set_off[seed];
         const uint32_t d = static_cast<uint32_t>(P.set_off[seed + 1] - so);
-        const uint32_t shift = bucket_shift(d, kCMaxBits);
-        // table + row info (blocked: thread t owns set elements PER*t ..)
-        uint32_t nb[PER];
+        const uint32_t* row = P.set_adj + so;
+        const WinGeom g = win_geom(CFG::kBitsA, CFG::kBitsB, P.bm_shrink, __ldg(row), __ldg(row + d - 1));
+        // bitmap + row table (blocked: thread t owns set elements PER*t ..)
+        uint32_t nc[PER];
         uint64_t ro[PER];
         uint32_t len[PER];
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
             const uint32_t i = threadIdx.x * PER + k;
-            nb[k] = 0;
+            nc[k] = 0;
             ro[k] = 0;
             len[k] = 0;
             if (i < d) {
-                const uint32_t x = __ldg(P.set_adj + so + i);
-                bucket_insert(T, shift, x);
+                const uint32_t x = __ldg(row + i);
+                win_set(bma, bmb, g, x);
                 ro[k] = P.out_off[x];
                 len[k] = static_cast<uint32_t>(P.out_off[x + 1] - ro[k]);
-                nb[k] = (len[k] + 31u) >> 5;
+                nc[k] = row_chunks(ro[k], len[k]);
             }
         }
         uint32_t agg;
-        BS(scan_tmp).ExclusiveSum(nb, nb, agg);
+        BS(scan_tmp).ExclusiveSum(nc, nc, agg);
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
             const uint32_t i = threadIdx.x * PER + k;
             if (i < d)
                 sts128(rows + 16u * i, make_uint4(static_cast<uint32_t>(ro[k]), static_cast<uint32_t>(ro[k] >> 32),
-                                                  len[k], nb[k]));
+                                                  len[k], nc[k]));
         }
-        if (threadIdx.x == 0) total_blocks = agg;
+        if (threadIdx.x == 0) total_chunks = agg;
         __syncthreads();
-        const uint32_t nblocks = total_blocks;
-        dispatch_probe(T, shift, *T.nstash, P.set_adj + so, d, P.variant, [&](const auto& probe) {
-            cta_blocks<ALGO, F, CFG>(P, seed, so, d, rows, nblocks, probe, sink);
+        const uint32_t nchunks = total_chunks;
+        with_win_probe(P, smem_addr(bma), smem_addr(bmb), g, RowVerify{row, d}, [&](const auto& probe) {
+            // equal, contiguous share of the seed's chunks per warp
+            const unsigned warp = threadIdx.x >> 5;
+            const uint32_t gb = static_cast<uint32_t>((static_cast<uint64_t>(nchunks) * warp) / CFG::kWarps);
+            const uint32_t ge = static_cast<uint32_t>((static_cast<uint64_t>(nchunks) * (warp + 1)) / CFG::kWarps);
+            if (gb < ge) {
+                CtaRowCursor cur(rows, row, d, gb, ge);
+                unsigned hits = 0;
+                stream_quads<ALGO, F>(P, seed, cur, probe, sink, hits);
+                sink.cnt += hits;
+            }
         });
         sink.end_unit(P, seed);
         __syncthreads();
-        for (uint32_t k = threadIdx.x; k < d; k += kCThreads) bucket_clear(T, shift, __ldg(P.set_adj + so + k));
-        if (threadIdx.x == 0) *T.nstash = 0;
+        for (uint32_t k = threadIdx.x; k < d; k += kCThreads) win_clear(bma, bmb, g, __ldg(row + k));
     }
     sink.flush(P);
 }
@@ -814,10 +855,10 @@ template <int ALGO, unsigned F>
 __global__ void __launch_bounds__(kGThreads) k_list_giant(ListParams P) {
     extern __shared__ __align__(16) unsigned char dsm[];
     __shared__ unsigned unit;
-    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+    const unsigned warp = threadIdx.x >> 5;
     uint32_t* bm = P.bitmaps + (uint64_t)blockIdx.x * P.bitmap_words;
     Sink<ALGO, F> sink;
-    attach_scratch(sink, dsm, kGWarps);
+    attach_scratch(sink, dsm);
     for (;;) {
         __syncthreads();
         if (threadIdx.x == 0) unit = atomicAdd(P.queue, 1u);
@@ -825,6 +866,7 @@ __global__ void __launch_bounds__(kGThreads) k_list_giant(ListParams P) {
         const unsigned u = unit;
         if (u >= P.nseeds) break;
         const uint32_t seed = P.seeds[u];
+        sink.begin_unit(P, seed);
         const uint64_t so = P.set_off[seed];
         const uint32_t d = static_cast<uint32_t>(P.set_off[seed + 1] - so);
         for (uint32_t k = threadIdx.x; k < d; k += kGThreads) {
@@ -832,7 +874,7 @@ __global__ void __launch_bounds__(kGThreads) k_list_giant(ListParams P) {
             atomicOr(bm + (v >> 5), 1u << (v & 31));
         }
         __syncthreads();
-        BitmapProbe probe{bm};
+        const BitmapProbe probe{bm, P.n};
         scan_x_range<ALGO, F>(P, seed, so, warp * 32, d, kGWarps * 32, probe, sink);
         sink.end_unit(P, seed);
         __syncthreads();
@@ -845,9 +887,9 @@ __global__ void __launch_bounds__(kGThreads) k_list_giant(ListParams P) {
 }
 
 // dynamic shared memory per CTA of each class kernel
-template <unsigned F> constexpr size_t smem_reg() { return warp_scratch_bytes<F>(kRWarps); }
-template <unsigned F> constexpr size_t smem_hash_warp() { return warp_scratch_bytes<F>(kHWarps) + kHWarps * kHTableBytes; }
-template <unsigned F, class CFG> constexpr size_t smem_hash_cta() { return warp_scratch_bytes<F>(CFG::kWarps) + cta_table_bytes<CFG>() + cta_row_bytes<CFG>(); }
+template <unsigned F> constexpr size_t smem_reg() { return warp_scratch_bytes<F>(kRWarps) + kRWarps * kRBmBytes; }
+template <unsigned F> constexpr size_t smem_warp() { return warp_scratch_bytes<F>(kHWarps) + kHWarps * kHBmBytes; }
+template <unsigned F, class CFG> constexpr size_t smem_cta() { return warp_scratch_bytes<F>(CFG::kWarps) + cta_bitmap_bytes<CFG>() + cta_row_bytes<CFG>(); }
 template <unsigned F> constexpr size_t smem_giant() { return warp_scratch_bytes<F>(kGWarps); }
 
 // ---- seed classification --------------------------------------------------

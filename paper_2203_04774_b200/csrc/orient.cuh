@@ -189,6 +189,12 @@ __global__ void __launch_bounds__(256) k_cost(uint32_t n, const uint32_t* __rest
 }
 
 // max over rows of the out-degree (listing batch arithmetic is 32-bit).
+// Checksum sink table: hv[r] = vertex_hash(inv[r]) (common.cuh).
+__global__ void k_vertex_hash(uint32_t n, const uint32_t* __restrict__ inv, unsigned long long* __restrict__ hv) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n; r += stride) hv[r] = vertex_hash(inv[r]);
+}
+
 __global__ void k_maxdeg(uint32_t n, const uint32_t* __restrict__ deg, unsigned int* out) {
     uint32_t m = 0;
     for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n;

@@ -69,20 +69,16 @@ struct tl_ctx {
 
     uint32_t n = 0;
     uint64_t m = 0;
-    bool oriented = false, in_built = false;
+    bool oriented = false, in_built = false, hv_built = false;
     uint32_t max_out = 0;
     unsigned long long cost[4] = {0, 0, 0, 0};
     double h2d_ms = 0, orient_ms = 0;
 
-    DevBuf goff, gadj, rank, inv, radj, out_off, out_adj, in_off, in_adj, outdeg, indeg, lists, acc,
+    DevBuf goff, gadj, rank, inv, hv, radj, out_off, out_adj, in_off, in_adj, outdeg, indeg, lists, acc,
         vcount, tri, scan_part, bitmaps, small;
     bool have_vcounts = false, have_tri = false;
-    int variant = 0;        // probe flavour (TRIGPU_VARIANT), for A/B measurement
-#ifdef TRIGPU_HUB_WINDOW
-    uint32_t win_bits = 32;  // hub window on (capped per class); TRIGPU_WIN_BITS overrides
-#else
-    uint32_t win_bits = 0;   // no hub window in this build
-#endif
+    int variant = 0;         // probe flavour (TRIGPU_VARIANT), for A/B measurement
+    uint32_t bm_shrink = 0;  // TRIGPU_BM_SHRINK: smaller bitmaps (tests force the filter path)
     unsigned long long tri_count = 0;
 
     tl_status fail(tl_status st, const std::string& what) {
@@ -200,6 +196,7 @@ tl_status orient_core(tl_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* goff,
                       const uint32_t* rank) {
     ctx->oriented = false;
     ctx->in_built = false;
+    ctx->hv_built = false;
     ctx->have_vcounts = false;
     ctx->have_tri = false;
     ctx->n = n;
@@ -336,11 +333,11 @@ tl_status launch_cta(tl_ctx* ctx, ListParams p, uint32_t* list, unsigned count, 
     p.seeds = list;
     p.nseeds = count;
     p.queue = queue;
-    const size_t smem = smem_hash_cta<F, CFG>();
-    tl_status st = set_smem(ctx, k_list_hash_cta<ALGO, F, CFG>, smem);
+    const size_t smem = smem_cta<F, CFG>();
+    tl_status st = set_smem(ctx, k_list_cta<ALGO, F, CFG>, smem);
     if (st != TL_OK) return st;
-    const unsigned grid = std::min<unsigned>(count, resident_grid(ctx, k_list_hash_cta<ALGO, F, CFG>, CFG::kThreads, smem));
-    k_list_hash_cta<ALGO, F, CFG><<<grid, CFG::kThreads, smem, ctx->s>>>(p);
+    const unsigned grid = std::min<unsigned>(count, resident_grid(ctx, k_list_cta<ALGO, F, CFG>, CFG::kThreads, smem));
+    k_list_cta<ALGO, F, CFG><<<grid, CFG::kThreads, smem, ctx->s>>>(p);
     LAUNCHED();
     return TL_OK;
 }
@@ -389,11 +386,11 @@ tl_status launch_classes(tl_ctx* ctx, ListParams base, uint32_t* const lists[kCl
         p.seeds = lists[1];
         p.nseeds = h[1];
         p.queue = queues + 1;
-        const size_t smem = smem_hash_warp<F>();
-        if ((st = set_smem(ctx, k_list_hash_warp<ALGO, F>, smem)) != TL_OK) return st;
+        const size_t smem = smem_warp<F>();
+        if ((st = set_smem(ctx, k_list_warp<ALGO, F>, smem)) != TL_OK) return st;
         const unsigned grid = std::min<unsigned>(grid_for((uint64_t)h[1] * 32, kHWarps * 32, ~0u),
-                                                 resident_grid(ctx, k_list_hash_warp<ALGO, F>, kHWarps * 32, smem));
-        k_list_hash_warp<ALGO, F><<<grid, kHWarps * 32, smem, ctx->s>>>(p);
+                                                 resident_grid(ctx, k_list_warp<ALGO, F>, kHWarps * 32, smem));
+        k_list_warp<ALGO, F><<<grid, kHWarps * 32, smem, ctx->s>>>(p);
         LAUNCHED();
     }
     if (h[2]) {
@@ -454,7 +451,7 @@ TL_API tl_status tl_create(tl_ctx** out, int device) {
     ctx->device = device;
     ctx->sms = prop.multiProcessorCount;
     if (const char* v = std::getenv("TRIGPU_VARIANT")) ctx->variant = std::atoi(v);
-    if (const char* v = std::getenv("TRIGPU_WIN_BITS")) ctx->win_bits = (uint32_t)std::atoi(v);
+    if (const char* v = std::getenv("TRIGPU_BM_SHRINK")) ctx->bm_shrink = (uint32_t)std::atoi(v);
     if ((e = cudaSetDevice(device)) != cudaSuccess || (e = cudaStreamCreateWithFlags(&ctx->s, cudaStreamNonBlocking)) != cudaSuccess ||
         (e = cudaStreamCreateWithFlags(&ctx->s2, cudaStreamNonBlocking)) != cudaSuccess) {
         g_create_error = std::string("tl_create: ") + cudaGetErrorString(e);
@@ -501,6 +498,8 @@ static tl_status check_args(tl_ctx* ctx, uint32_t n, uint64_t m, const void* off
     ctx->launches = 0;
     if ((n && (!off || !rank)) || (m && !adj)) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "orient: null input pointer");
     if (n == 0xFFFFFFFFu) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "orient: n must be < 2^32 - 1 (VertexId, common.hpp:11-13)");
+    if (n > 0xFFF00000u)  // the listing pads partial quads with kNone, which must lie 2^20 above every rank
+        return ctx->fail(TL_ERR_INVALID_ARGUMENT, "orient: n > 2^32 - 2^20 is not supported by the listing engine");
     if (m > (uint64_t)n * (n ? n - 1 : 0) / 2) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "orient: m exceeds n(n-1)/2");
     if (cudaSetDevice(ctx->device) != cudaSuccess) return ctx->cuda_fail("cudaSetDevice", cudaGetLastError());
     return TL_OK;
@@ -570,10 +569,21 @@ TL_API tl_status tl_list(tl_ctx* ctx, int algo, unsigned out_flags, tl_stats* ou
     base.out_off = P<uint64_t>(ctx->out_off);
     base.out_adj = P<uint32_t>(ctx->out_adj);
     base.inv = P<uint32_t>(ctx->inv);
+    if ((out_flags & TL_OUT_CHECKSUM) && !ctx->hv_built) {
+        // checksum sink: h(dense id) per rank, once per orientation
+        ENSURE(hv, (size_t)std::max<uint32_t>(n, 1) * 8);
+        if (n) {
+            k_vertex_hash<<<grid_for(n, 256, ctx->sms * 16), 256, 0, ctx->s>>>(n, P<uint32_t>(ctx->inv),
+                                                                              P<unsigned long long>(ctx->hv));
+            LAUNCHED();
+        }
+        ctx->hv_built = true;
+    }
+    base.hv = P<unsigned long long>(ctx->hv);
     base.acc = acc;
     base.vcount = want_vc ? P<unsigned long long>(ctx->vcount) : nullptr;
     base.variant = ctx->variant;
-    base.win_bits = ctx->win_bits;
+    base.bm_shrink = ctx->bm_shrink;
 
     CK(cudaEventRecord(ctx->ev[PH_COUNT + 3], ctx->s));
     CK(cudaMemsetAsync(counts, 0, 16 * sizeof(unsigned int), ctx->s));

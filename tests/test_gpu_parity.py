@@ -266,13 +266,14 @@ def test_full_size_c4_properties(ctx):
         assert v[0] == vals[0][0] and v[1] == vals[0][1] and np.array_equal(v[2], vals[0][2])
 
 
-@pytest.mark.parametrize("win_bits", [1, 6, 11])
-def test_probe_window_split(monkeypatch, win_bits):
-    """The class H / C probe splits each seed's set between a hub-window
-    bitmap and a hash table. Shrinking the window (TRIGPU_WIN_BITS) forces
-    the hash path on graphs small enough for the oracle; results must not
-    depend on where the split falls."""
-    monkeypatch.setenv("TRIGPU_WIN_BITS", str(win_bits))
+@pytest.mark.parametrize("shrink", [4, 8, 13])
+def test_probe_filter_path(monkeypatch, shrink):
+    """Each seed's set is a windowed bitmap: exact when the set's rank span
+    fits, otherwise a filter whose candidates are verified exactly.
+    Shrinking every class's bitmap (TRIGPU_BM_SHRINK) pushes the seeds of
+    graphs small enough for the oracle through the filter + verification path
+    with many false positives; results must not change."""
+    monkeypatch.setenv("TRIGPU_BM_SHRINK", str(shrink))
     c = tg.Context(0)
     try:
         for g in (tg.gen_rmat(15, 16, 3), tg.gen_chung_lu(50000, 800000, seed=4)):

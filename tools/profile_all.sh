@@ -14,13 +14,13 @@ prof() {  # name regex skip
       -o gpurun_out/prof_${TAG}_$1 $CMD > gpurun_out/ncu_full_${TAG}_$1.log 2>&1
 }
 prof reg k_list_reg 0
-prof hash_warp k_list_hash_warp 0
-prof cta_c1 k_list_hash_cta 0
-prof cta_c2 k_list_hash_cta 1
+prof warp k_list_warp 0
+prof cta_c1 k_list_cta 0
+prof cta_c2 k_list_cta 1
 echo "profile_all done"
 # export summaries on the box and drop the big .ncu-rep files (gpurun brings
 # back at most 64 MiB of gpurun_out/)
-for k in reg hash_warp cta_c1 cta_c2; do
+for k in reg warp cta_c1 cta_c2; do
   R=gpurun_out/prof_${TAG}_$k.ncu-rep
   [ -f "$R" ] || continue
   ncu -i $R --page raw --csv > gpurun_out/raw_${TAG}_$k.csv 2>/dev/null

@@ -20,7 +20,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "gpurun_out")
 PROF = os.path.join(ROOT, "profiles")
-KERNELS = ["reg", "hash_warp", "cta_c1", "cta_c2"]
+KERNELS = ["reg", "warp", "cta_c1", "cta_c2"]
 METRICS = [
     ("gpu__time_duration.sum", "time"),
     ("dram__bytes_read.sum", "DRAM read"),
