@@ -214,11 +214,21 @@ tl_status orient_core(tl_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* goff,
 
     CK(cudaMemsetAsync(ctx->inv.p, 0xFF, (size_t)n * 4, ctx->s));
     CK(cudaMemsetAsync(flags, 0, 64, ctx->s));
+    // rows of >= kLongDeg edges (one CTA each): list in the free part of
+    // `lists` (the sort classes use its first 3n words), count + two queues
+    uint32_t* long_rows = P<uint32_t>(ctx->lists) + 3 * (uint64_t)n;
+    auto* long_cnt = reinterpret_cast<unsigned int*>(flags + 8);  // [0] count, [1] [2] queues
+    CK(cudaMemsetAsync(long_cnt, 0, 16, ctx->s));
     if (n) {
         k_inverse<<<grid_for(n, 256, big), 256, 0, ctx->s>>>(n, rank, P<uint32_t>(ctx->inv), flags);
         LAUNCHED();
-        k_relabel_count<<<grid_for((uint64_t)n * 32, 256, big * 2), 256, 0, ctx->s>>>(
-            n, goff, gadj, rank, P<uint32_t>(ctx->radj), P<uint32_t>(ctx->outdeg), P<uint32_t>(ctx->indeg), flags);
+        k_relabel_count<<<grid_for((uint64_t)n, 256, big * 2), 256, 0, ctx->s>>>(
+            n, goff, gadj, rank, P<uint32_t>(ctx->radj), P<uint32_t>(ctx->outdeg), P<uint32_t>(ctx->indeg),
+            long_rows, long_cnt, flags);
+        LAUNCHED();
+        k_relabel_long<<<ctx->sms * 2, kLongThreads, 0, ctx->s>>>(n, goff, gadj, rank, P<uint32_t>(ctx->radj),
+                                                                  P<uint32_t>(ctx->outdeg), P<uint32_t>(ctx->indeg),
+                                                                  long_rows, long_cnt, long_cnt + 1, flags);
         LAUNCHED();
     }
     CK(cudaEventRecord(ctx->ev[PH_RELABEL], ctx->s));
@@ -232,9 +242,12 @@ tl_status orient_core(tl_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* goff,
     if (st != TL_OK) return st;
     CK(cudaEventRecord(ctx->ev[PH_SCAN], ctx->s));
     if (n) {
-        k_scatter<false><<<grid_for((uint64_t)n * 32, 256, big * 2), 256, 0, ctx->s>>>(
-            n, goff, P<uint32_t>(ctx->radj), rank, P<uint64_t>(ctx->out_off), P<uint32_t>(ctx->out_adj), nullptr,
-            nullptr);
+        k_scatter<<<grid_for((uint64_t)n, 256, big * 2), 256, 0, ctx->s>>>(
+            n, goff, P<uint32_t>(ctx->radj), rank, P<uint64_t>(ctx->out_off), P<uint32_t>(ctx->out_adj));
+        LAUNCHED();
+        k_scatter_long<<<ctx->sms * 2, kLongThreads, 0, ctx->s>>>(goff, P<uint32_t>(ctx->radj), rank,
+                                                                  P<uint64_t>(ctx->out_off), P<uint32_t>(ctx->out_adj),
+                                                                  long_rows, long_cnt, long_cnt + 2);
         LAUNCHED();
     }
     CK(cudaEventRecord(ctx->ev[PH_SCATTER], ctx->s));

@@ -1,7 +1,7 @@
 #!/bin/bash
 # Per-launch device times of one bench step (tools/launchlist.sh <config> <tag>)
-CFG=${1:-c4}; TAG=${2:-x}
-CMD="python bench.py --config $CFG --steps 1 --warmup 1 --no-cpu-baseline"
+CFG=${1:-c4}; TAG=${2:-x}; EXTRA=${3:-}
+CMD="python bench.py --config $CFG --steps 1 --warmup 1 --no-cpu-baseline $EXTRA"
 mkdir -p gpurun_out
 $CMD > gpurun_out/plain_$TAG.json 2> gpurun_out/plain_$TAG.err && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv \
