@@ -38,9 +38,11 @@ enum : int { ALGO_APP = 0, ALGO_APM = 1 };
 
 struct ListParams {
     uint32_t n;
-    const uint64_t* set_off;  // probe-set rows: out-CSR (A+-) or in-CSR (A++)
+    const uint64_t* set_off;  // probe-set rows: out-CSR (A+-) or in-CSR (A++): start, length
+    const uint32_t* set_len;
     const uint32_t* set_adj;
-    const uint64_t* out_off;  // scanned rows: always the out-CSR
+    const uint64_t* out_off;  // scanned rows: always the out-CSR, rows padded to quads (starts
+    const uint32_t* out_len;  //   are multiples of 4, pad slots hold kNone)
     const uint32_t* out_adj;
     const uint32_t* inv;      // rank -> dense id
     const unsigned long long* hv;  // rank -> vertex_hash(dense id) (checksum sink)
@@ -174,7 +176,10 @@ struct BitmapProbe {
     static constexpr bool low = false;
     const uint32_t* bm;
     uint32_t n;  // bits n .. are the always-zero slack words
-    __device__ __forceinline__ uint32_t bit(uint32_t y) const { return (__ldcg(bm + (y >> 5)) >> (y & 31)) & 1u; }
+    __device__ __forceinline__ uint32_t bit(uint32_t y) const {
+        y = min(y, n);  // pad slots (kNone) read the zero slack
+        return (__ldcg(bm + (y >> 5)) >> (y & 31)) & 1u;
+    }
     __device__ __forceinline__ bool below(uint32_t) const { return false; }
     __device__ __forceinline__ uint32_t cand(uint32_t) const { return 0u; }
     __device__ __forceinline__ bool verify(uint32_t, bool act) const { return act; }
@@ -316,70 +321,56 @@ struct Sink {
 };
 
 // ---- row streaming -------------------------------------------------------------
-// Long rows are read as 128-element CHUNKS of 16-byte quads: lane l loads
-// quad qb + l (ld.global.nc.v4: four elements), a warp load is 512 contiguous
-// bytes, and four chunks' loads are issued back to back in one asm block
-// (ldg4q), so a warp keeps 2 KB in flight. Chunk c of a row starting at
-// element s covers quads (s >> 2) + 32c ..; the few elements of the first and
-// last quad outside the row are replaced by the probe's sentinel. The chunks
-// come from a Cursor (rows held by the lanes, or a CTA's shared row table),
-// four at a time; one batch may span several rows.
+// Out-rows are padded to whole 16-byte quads (pad slots hold kNone, which
+// never hits), so long rows are read as 128-element CHUNKS of quads: lane l
+// loads quad qb + l (ld.global.nc.v4: four elements), a warp load is 512
+// contiguous bytes, and four chunks' loads are issued back to back in one asm
+// block (ldg4q): a warp keeps 2 KB in flight. Lanes past the row's last quad
+// are predicated off and their bits masked. The chunks come from a Cursor
+// (rows held by the lanes, or a CTA's shared row table), four at a time; one
+// batch may span several rows.
 constexpr uint32_t kLongRow = 96;  // rows at least this long are read in quad chunks
 constexpr int kQU = 4;             // chunks per batch
 
 struct Chunk {
-    uint64_t qb;  // first quad (global quad index into out_adj)
-    int32_t r0;   // row-relative element index of lane 0's first element (-3 .. )
-    uint32_t len; // row length
+    uint32_t qb;  // first quad (global quad index into out_adj)
+    uint32_t nq;  // quads of the row in this chunk (0 = no chunk)
     uint32_t x;   // row owner (sinks)
-    bool valid;
 };
 
-__device__ __forceinline__ uint32_t row_chunks(uint64_t ro, uint32_t len) {
-    return len ? (static_cast<uint32_t>(ro & 3u) + len + 127u) >> 7 : 0u;
-}
+// chunks of a row of nqr quads
+__device__ __forceinline__ uint32_t row_chunks(uint32_t nqr) { return (nqr + 31u) >> 5; }
 
-template <int ALGO, unsigned F, class Probe, class Cursor>
+template <int ALGO, unsigned F, bool kSparse, class Probe, class Cursor>
 __device__ __forceinline__ void stream_quads(const ListParams& P, uint32_t seed, Cursor& cur, const Probe& probe,
                                              Sink<ALGO, F>& sink, unsigned& hits) {
     const unsigned lane = lane_id();
     const uint4* const quads = reinterpret_cast<const uint4*>(P.out_adj);
-    const uint32_t sent = probe.sentinel();
     // chunks per batch: 4 (2 KB in flight per warp); 2 for the buffered sinks,
     // whose batch / drain code would otherwise spill
     constexpr int QU = Sink<ALGO, F>::kBuffered ? 2 : kQU;
+    uint4 y[QU];
+#pragma unroll
+    for (int i = 0; i < QU; ++i) y[i] = make_uint4(kNone, kNone, kNone, kNone);
     while (cur.more()) {
         Chunk ch[QU];
         cur.next(ch);
         const uint4* a[QU];
         bool pr[QU];
-        uint4 y[QU];
-        int32_t r[QU];
 #pragma unroll
         for (int i = 0; i < QU; ++i) {
-            r[i] = ch[i].r0 + 4 * static_cast<int32_t>(lane);
-            pr[i] = ch[i].valid && r[i] < static_cast<int32_t>(ch[i].len);
-            a[i] = quads + ch[i].qb + lane;
-            y[i] = make_uint4(sent, sent, sent, sent);
+            pr[i] = lane < ch[i].nq;
+            a[i] = quads + (ch[i].qb + lane);
         }
         ldgq(a, pr, y);
-#pragma unroll
-        for (int i = 0; i < QU; ++i) {
-            // partial first / last quad of a row: blank the elements outside it
-            if (pr[i] && (r[i] < 0 || static_cast<uint32_t>(r[i] + 4) > ch[i].len)) {
-                if (static_cast<uint32_t>(r[i]) >= ch[i].len) y[i].x = sent;
-                if (static_cast<uint32_t>(r[i] + 1) >= ch[i].len) y[i].y = sent;
-                if (static_cast<uint32_t>(r[i] + 2) >= ch[i].len) y[i].z = sent;
-                if (static_cast<uint32_t>(r[i] + 3) >= ch[i].len) y[i].w = sent;
-            }
-        }
         uint32_t hb[QU];
         bool any = false;
 #pragma unroll
         for (int i = 0; i < QU; ++i) {
             hb[i] = probe.bit(y[i].x) | (probe.bit(y[i].y) << 1) | (probe.bit(y[i].z) << 2) | (probe.bit(y[i].w) << 3);
+            hb[i] = pr[i] ? hb[i] : 0u;
             if constexpr (Probe::low)
-                any |= probe.below(y[i].x) | probe.below(y[i].y) | probe.below(y[i].z) | probe.below(y[i].w);
+                any |= pr[i] && (probe.below(y[i].x) | probe.below(y[i].y) | probe.below(y[i].z) | probe.below(y[i].w));
         }
         if constexpr (Probe::low) {
             // elements below the window: region-B candidates, verified here
@@ -389,7 +380,7 @@ __device__ __forceinline__ void stream_quads(const ListParams& P, uint32_t seed,
                     const uint32_t e[4] = {y[i].x, y[i].y, y[i].z, y[i].w};
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
-                        const bool c = probe.below(e[k]) && probe.cand(e[k]);
+                        const bool c = pr[i] && probe.below(e[k]) && probe.cand(e[k]);
                         if (__any_sync(FULL, c))
                             if (probe.verify(e[k], c)) hb[i] |= 1u << k;
                     }
@@ -419,36 +410,34 @@ __device__ __forceinline__ void stream_quads(const ListParams& P, uint32_t seed,
             // h(s) h(x). Straight-line predicated gathers (hub ranks: L1/L2
             // hits), all in flight before the first use.
             if (__any_sync(FULL, hm != 0)) {
+                const unsigned long long* const hv = P.hv;
                 unsigned long long sy[QU];
 #pragma unroll
                 for (int i = 0; i < QU; ++i) {
-                    const unsigned long long a0 = (hb[i] & 1u) ? __ldg(P.hv + y[i].x) : 0ull;
-                    const unsigned long long a1 = (hb[i] & 2u) ? __ldg(P.hv + y[i].y) : 0ull;
-                    const unsigned long long a2 = (hb[i] & 4u) ? __ldg(P.hv + y[i].z) : 0ull;
-                    const unsigned long long a3 = (hb[i] & 8u) ? __ldg(P.hv + y[i].w) : 0ull;
+                    const unsigned long long a0 = (hb[i] & 1u) ? __ldg(hv + y[i].x) : 0ull;
+                    const unsigned long long a1 = (hb[i] & 2u) ? __ldg(hv + y[i].y) : 0ull;
+                    const unsigned long long a2 = (hb[i] & 4u) ? __ldg(hv + y[i].z) : 0ull;
+                    const unsigned long long a3 = (hb[i] & 8u) ? __ldg(hv + y[i].w) : 0ull;
                     sy[i] = (a0 + a1) + (a2 + a3);
                 }
 #pragma unroll
                 for (int i = 0; i < QU; ++i)
-                    if (hb[i]) sink.sum += sy[i] * (sink.hs * __ldg(P.hv + ch[i].x));
+                    if (hb[i]) sink.sum += sy[i] * (sink.hs * __ldg(hv + ch[i].x));
             }
         }
     }
 }
 
-// Rows held by the lanes (lane j: row of x_j at ro, rl elements); the cursor
-// visits the rows selected by `mask` in lane order, chunk by chunk. Four
-// chunks of one row are handed out at once when the row has them left.
+// Rows held by the lanes (lane j: row of x_j, first quad q0, nqr quads); the
+// cursor visits the rows selected by `mask` in lane order, chunk by chunk.
+// N chunks of one row are handed out at once when the row has them left.
 struct LaneRowCursor {
-    uint64_t ro;
-    uint32_t rl, xl;  // this lane's row
-    unsigned left;    // rows not started yet
-    uint64_t q0;      // current row (uniform): first quad
-    int32_t h;        // s & 3
-    uint32_t len, x, c, nch;
+    uint32_t q0l, nql, xl;  // this lane's row
+    unsigned left;          // rows not started yet
+    uint32_t q0, nqr, x, c, nch;  // current row (uniform)
     bool on;
-    __device__ __forceinline__ LaneRowCursor(uint64_t ro_, uint32_t rl_, uint32_t x_, unsigned mask)
-        : ro(ro_), rl(rl_), xl(x_), left(mask), q0(0), h(0), len(0), x(0), c(0), nch(0), on(false) {
+    __device__ __forceinline__ LaneRowCursor(uint32_t q0_, uint32_t nq_, uint32_t x_, unsigned mask)
+        : q0l(q0_), nql(nq_), xl(x_), left(mask), q0(0), nqr(0), x(0), c(0), nch(0), on(false) {
         advance();
     }
     __device__ __forceinline__ void advance() {
@@ -456,18 +445,14 @@ struct LaneRowCursor {
         if (!on) return;
         const int j = __ffs(left) - 1;
         left &= left - 1;
-        const uint64_t s = shfl64(ro, j);
-        len = __shfl_sync(FULL, rl, j);
+        q0 = __shfl_sync(FULL, q0l, j);
+        nqr = __shfl_sync(FULL, nql, j);
         x = __shfl_sync(FULL, xl, j);
-        q0 = s >> 2;
-        h = static_cast<int32_t>(s & 3u);
         c = 0;
-        nch = (static_cast<uint32_t>(h) + len + 127u) >> 7;
+        nch = row_chunks(nqr);
     }
     __device__ __forceinline__ bool more() const { return on; }
-    __device__ __forceinline__ Chunk at(uint32_t cc) const {
-        return Chunk{q0 + 32u * cc, static_cast<int32_t>(128u * cc) - h, len, x, true};
-    }
+    __device__ __forceinline__ Chunk at(uint32_t cc) const { return Chunk{q0 + 32u * cc, min(32u, nqr - 32u * cc), x}; }
     template <int N>
     __device__ __forceinline__ void next(Chunk (&ch)[N]) {
         if (c + N <= nch) {  // fast path: N chunks of the current row
@@ -483,45 +468,37 @@ struct LaneRowCursor {
                 ch[i] = at(c);
                 if (++c == nch) advance();
             } else {
-                ch[i] = Chunk{0, 0, 0, 0, false};
+                ch[i] = Chunk{0, 0, 0};
             }
         }
     }
 };
 
 // A warp's contiguous range [g, ge) of a CTA seed's chunks (shared row table
-// {ro lo, ro hi, len, first chunk}), walked forward row by row.
+// {first quad, quads, first chunk, x}), walked forward row by row.
 struct CtaRowCursor {
     unsigned rows;
-    const uint32_t* xs;  // the seed's set row: x of row i
-    uint32_t g, ge, i, rf, rend, x, len;
-    uint64_t q0;
-    int32_t h;
-    __device__ __forceinline__ CtaRowCursor(unsigned rows_, const uint32_t* xs_, uint32_t d, uint32_t gb, uint32_t ge_)
-        : rows(rows_), xs(xs_), g(gb), ge(ge_) {
+    uint32_t g, ge, i, rend;
+    uint4 r;  // current row's entry
+    __device__ __forceinline__ CtaRowCursor(unsigned rows_, uint32_t d, uint32_t gb, uint32_t ge_)
+        : rows(rows_), g(gb), ge(ge_) {
         uint32_t lo = 0, hi = d - 1;
         while (lo < hi) {  // last row i with first_chunk(i) <= gb
             const uint32_t mid = (lo + hi + 1) >> 1;
-            if (lds32(rows + 16u * mid + 12u) <= gb) lo = mid;
+            if (lds32(rows + 16u * mid + 8u) <= gb) lo = mid;
             else hi = mid - 1;
         }
         i = lo;
         load();
     }
     __device__ __forceinline__ void load() {
-        const uint4 r = lds128(rows + 16u * i);
-        const uint64_t ro = (static_cast<uint64_t>(r.y) << 32) | r.x;
-        len = r.z;
-        rf = r.w;
-        rend = rf + row_chunks(ro, len);
-        q0 = ro >> 2;
-        h = static_cast<int32_t>(r.x & 3u);
-        x = __ldg(xs + i);
+        r = lds128(rows + 16u * i);
+        rend = r.z + row_chunks(r.y);
     }
     __device__ __forceinline__ bool more() const { return g < ge; }
     __device__ __forceinline__ Chunk at(uint32_t gg) const {
-        const uint32_t cc = gg - rf;
-        return Chunk{q0 + 32u * cc, static_cast<int32_t>(128u * cc) - h, len, x, true};
+        const uint32_t cc = gg - r.z;
+        return Chunk{r.x + 32u * cc, min(32u, r.y - 32u * cc), r.w};
     }
     template <int N>
     __device__ __forceinline__ void next(Chunk (&ch)[N]) {
@@ -541,7 +518,7 @@ struct CtaRowCursor {
                 ch[k] = at(g);
                 ++g;
             } else {
-                ch[k] = Chunk{0, 0, 0, 0, false};
+                ch[k] = Chunk{0, 0, 0};
             }
         }
     }
@@ -561,13 +538,13 @@ __device__ __forceinline__ void scan_rows(const ListParams& P, uint32_t seed, ui
     uint32_t rl = 0;
     if (xvalid) {
         ro = P.out_off[x];
-        rl = static_cast<uint32_t>(P.out_off[x + 1] - ro);
+        rl = P.out_len[x];
     }
     unsigned hits = 0;
     // ---- phase 1: long rows, quad chunks
     {
-        LaneRowCursor cur(ro, rl, x, __ballot_sync(FULL, rl >= kLongRow));
-        stream_quads<ALGO, F>(P, seed, cur, probe, sink, hits);
+        LaneRowCursor cur(static_cast<uint32_t>(ro >> 2), (rl + 3u) >> 2, x, __ballot_sync(FULL, rl >= kLongRow));
+        stream_quads<ALGO, F, true>(P, seed, cur, probe, sink, hits);
     }
     if (rl >= kLongRow) rl = 0;
     // ---- phase 2: short rows
@@ -693,7 +670,7 @@ __global__ void __launch_bounds__(kRWarps * 32, TRIGPU_WARP_MINB) k_list_reg(Lis
         const uint32_t seed = P.seeds[i];
         sink.begin_unit(P, seed);
         const uint64_t so = P.set_off[seed];
-        const uint32_t d = static_cast<uint32_t>(P.set_off[seed + 1] - so);
+        const uint32_t d = P.set_len[seed];
         const uint32_t s = lane < d ? __ldg(P.set_adj + so + lane) : kNone;
         const WinGeom g = win_geom(kRBitsA, kRBitsB, P.bm_shrink, __shfl_sync(FULL, s, 0), __shfl_sync(FULL, s, d - 1));
         if (lane < d) win_set(bma, bmb, g, s);
@@ -732,7 +709,7 @@ __global__ void __launch_bounds__(kHWarps * 32, TRIGPU_WARP_MINB) k_list_warp(Li
         const uint32_t seed = P.seeds[i];
         sink.begin_unit(P, seed);
         const uint64_t so = P.set_off[seed];
-        const uint32_t d = static_cast<uint32_t>(P.set_off[seed + 1] - so);
+        const uint32_t d = P.set_len[seed];
         const uint32_t* row = P.set_adj + so;
         const WinGeom g = win_geom(kHBitsA, kHBitsB, P.bm_shrink, __ldg(row), __ldg(row + d - 1));
         for (uint32_t k = lane; k < d; k += 32) win_set(bma, bmb, g, __ldg(row + k));
@@ -769,7 +746,7 @@ using CfgC2 = CtaCfg<1024, 19, 15, 4096, 1>;
 template <class CFG>
 constexpr size_t cta_bitmap_bytes() { return win_bytes(CFG::kBitsA, CFG::kBitsB); }
 template <class CFG>
-constexpr size_t cta_row_bytes() { return CFG::kMaxD * 16; }  // uint4 {ro lo, ro hi, len, first chunk}
+constexpr size_t cta_row_bytes() { return CFG::kMaxD * 16; }  // uint4 {first quad, quads, first chunk, x}
 
 template <int ALGO, unsigned F, class CFG>
 __global__ void __launch_bounds__(CFG::kThreads, CFG::kMinBlocks) k_list_cta(ListParams P) {
@@ -795,25 +772,25 @@ __global__ void __launch_bounds__(CFG::kThreads, CFG::kMinBlocks) k_list_cta(Lis
         const uint32_t seed = P.seeds[u];
         sink.begin_unit(P, seed);
         const uint64_t so = P.set_off[seed];
-        const uint32_t d = static_cast<uint32_t>(P.set_off[seed + 1] - so);
+        const uint32_t d = P.set_len[seed];
         const uint32_t* row = P.set_adj + so;
         const WinGeom g = win_geom(CFG::kBitsA, CFG::kBitsB, P.bm_shrink, __ldg(row), __ldg(row + d - 1));
         // bitmap + row table (blocked: thread t owns set elements PER*t ..)
-        uint32_t nc[PER];
-        uint64_t ro[PER];
-        uint32_t len[PER];
+        uint32_t nc[PER], q0[PER], nq[PER], xs[PER];
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
             const uint32_t i = threadIdx.x * PER + k;
             nc[k] = 0;
-            ro[k] = 0;
-            len[k] = 0;
+            q0[k] = 0;
+            nq[k] = 0;
+            xs[k] = 0;
             if (i < d) {
                 const uint32_t x = __ldg(row + i);
                 win_set(bma, bmb, g, x);
-                ro[k] = P.out_off[x];
-                len[k] = static_cast<uint32_t>(P.out_off[x + 1] - ro[k]);
-                nc[k] = row_chunks(ro[k], len[k]);
+                xs[k] = x;
+                q0[k] = static_cast<uint32_t>(P.out_off[x] >> 2);
+                nq[k] = (P.out_len[x] + 3u) >> 2;
+                nc[k] = row_chunks(nq[k]);
             }
         }
         uint32_t agg;
@@ -821,9 +798,7 @@ __global__ void __launch_bounds__(CFG::kThreads, CFG::kMinBlocks) k_list_cta(Lis
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
             const uint32_t i = threadIdx.x * PER + k;
-            if (i < d)
-                sts128(rows + 16u * i, make_uint4(static_cast<uint32_t>(ro[k]), static_cast<uint32_t>(ro[k] >> 32),
-                                                  len[k], nc[k]));
+            if (i < d) sts128(rows + 16u * i, make_uint4(q0[k], nq[k], nc[k], xs[k]));
         }
         if (threadIdx.x == 0) total_chunks = agg;
         __syncthreads();
@@ -834,9 +809,9 @@ __global__ void __launch_bounds__(CFG::kThreads, CFG::kMinBlocks) k_list_cta(Lis
             const uint32_t gb = static_cast<uint32_t>((static_cast<uint64_t>(nchunks) * warp) / CFG::kWarps);
             const uint32_t ge = static_cast<uint32_t>((static_cast<uint64_t>(nchunks) * (warp + 1)) / CFG::kWarps);
             if (gb < ge) {
-                CtaRowCursor cur(rows, row, d, gb, ge);
+                CtaRowCursor cur(rows, d, gb, ge);
                 unsigned hits = 0;
-                stream_quads<ALGO, F>(P, seed, cur, probe, sink, hits);
+                stream_quads<ALGO, F, false>(P, seed, cur, probe, sink, hits);
                 sink.cnt += hits;
             }
         });
@@ -868,7 +843,7 @@ __global__ void __launch_bounds__(kGThreads) k_list_giant(ListParams P) {
         const uint32_t seed = P.seeds[u];
         sink.begin_unit(P, seed);
         const uint64_t so = P.set_off[seed];
-        const uint32_t d = static_cast<uint32_t>(P.set_off[seed + 1] - so);
+        const uint32_t d = P.set_len[seed];
         for (uint32_t k = threadIdx.x; k < d; k += kGThreads) {
             const uint32_t v = __ldg(P.set_adj + so + k);
             atomicOr(bm + (v >> 5), 1u << (v & 31));
@@ -900,7 +875,7 @@ struct SeedLists {
     unsigned int* counts;     // [kClasses]
 };
 
-__global__ void __launch_bounds__(256) k_classify_seeds(uint32_t n, const uint64_t* __restrict__ set_off,
+__global__ void __launch_bounds__(256) k_classify_seeds(uint32_t n, const uint32_t* __restrict__ set_len,
                                                         SeedLists L) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const uint64_t start = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -908,7 +883,7 @@ __global__ void __launch_bounds__(256) k_classify_seeds(uint32_t n, const uint64
     for (uint64_t t = 0; t < trips; ++t) {
         const uint64_t r = start + t * stride;
         uint64_t d = 0;
-        if (r < n) d = set_off[r + 1] - set_off[r];
+        if (r < n) d = set_len[r];
         int cls = -1;
         if (d >= 2) cls = d <= 32 ? 0 : d <= 256 ? 1 : d <= CfgC1::kMaxD ? 2 : d <= CfgC2::kMaxD ? 3 : 4;
 #pragma unroll

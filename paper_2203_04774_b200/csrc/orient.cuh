@@ -294,7 +294,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_apply(uint32_t n, const u
 // free: rows are sorted afterwards). Same row layout as k_relabel_count.
 __global__ void __launch_bounds__(256) k_scatter(uint32_t n, const uint64_t* __restrict__ goff,
                                                  const uint32_t* __restrict__ radj, const uint32_t* __restrict__ rank,
-                                                 const uint64_t* __restrict__ out_off, uint32_t* __restrict__ out_adj) {
+                                                 const uint64_t* __restrict__ out_off, const uint32_t* __restrict__ outdeg,
+                                                 uint32_t* __restrict__ out_adj) {
     __shared__ uint32_t cnt_sm[8][32];
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
     const unsigned lt = lanemask_lt();
@@ -312,6 +313,8 @@ __global__ void __launch_bounds__(256) k_scatter(uint32_t n, const uint64_t* __r
         if (deg && deg < kLongDeg) {
             ru = rank[u];
             op = out_off[ru];
+            // the row's pad slots (out-rows are padded to a multiple of 4: quads)
+            for (uint32_t k = outdeg[ru]; k & 3u; ++k) out_adj[op + k] = kNone;
         }
         const FlatRows f = flat_rows(b, deg < kLongDeg ? deg : 0u);
         const uint32_t cr = __shfl_sync(FULL, ru, f.src);
@@ -350,6 +353,7 @@ __global__ void __launch_bounds__(kLongThreads) k_scatter_long(const uint64_t* _
                                                                const uint32_t* __restrict__ radj,
                                                                const uint32_t* __restrict__ rank,
                                                                const uint64_t* __restrict__ out_off,
+                                                               const uint32_t* __restrict__ outdeg,
                                                                uint32_t* __restrict__ out_adj,
                                                                const uint32_t* __restrict__ long_rows,
                                                                const unsigned int* long_count, unsigned int* queue) {
@@ -368,6 +372,8 @@ __global__ void __launch_bounds__(kLongThreads) k_scatter_long(const uint64_t* _
         const uint64_t b = goff[u], e = goff[u + 1];
         const uint32_t ru = rank[u];
         const uint64_t op = out_off[ru];
+        if (threadIdx.x == 0)
+            for (uint32_t k = outdeg[ru]; k & 3u; ++k) out_adj[op + k] = kNone;  // pad slots
         // whole warps stride over the row (the loop bound is warp-uniform)
         const uint64_t wb = b + (threadIdx.x & ~31u);
         for (uint64_t i0 = wb; i0 < e; i0 += 4 * kLongThreads) {
@@ -421,10 +427,19 @@ __global__ void __launch_bounds__(256) k_cost(uint32_t n, const uint32_t* __rest
 }
 
 // max over rows of the out-degree (listing batch arithmetic is 32-bit).
+// Padded out-row lengths: rows start on 16-byte boundaries (quads) so the
+// listing reads them as whole quads; pad slots hold kNone.
+__global__ void k_pad_len(uint32_t n, const uint32_t* __restrict__ deg, uint32_t* __restrict__ plen) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n; r += stride)
+        plen[r] = (deg[r] + 3u) & ~3u;
+}
+
 // Checksum sink table: hv[r] = vertex_hash(inv[r]) (common.cuh).
 __global__ void k_vertex_hash(uint32_t n, const uint32_t* __restrict__ inv, unsigned long long* __restrict__ hv) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n; r += stride) hv[r] = vertex_hash(inv[r]);
+    for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r <= n; r += stride)
+        hv[r] = r < n ? vertex_hash(inv[r]) : 0ull;  // hv[n] = 0: the no-hit lanes' load target
 }
 
 __global__ void k_maxdeg(uint32_t n, const uint32_t* __restrict__ deg, unsigned int* out) {
@@ -456,13 +471,13 @@ __global__ void k_gather_u64(uint32_t n, const unsigned long long* __restrict__ 
 // Warp per dense row u: copy rank-space row rank[u], mapped to dense ids.
 __global__ void k_export_rows(uint32_t n, const uint32_t* __restrict__ rank,
                               const uint32_t* __restrict__ inv, const uint64_t* __restrict__ roff,
-                              const uint32_t* __restrict__ radj, const uint64_t* __restrict__ doff,
-                              uint32_t* __restrict__ dadj) {
+                              const uint32_t* __restrict__ rlen, const uint32_t* __restrict__ radj,
+                              const uint64_t* __restrict__ doff, uint32_t* __restrict__ dadj) {
     const unsigned lane = lane_id();
     const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t u = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; u < n; u += warps) {
         const uint32_t r = rank[u];
-        const uint64_t b = roff[r], e = roff[r + 1], d = doff[u];
+        const uint64_t b = roff[r], e = b + rlen[r], d = doff[u];
         for (uint64_t i = b + lane; i < e; i += 32) dadj[d + (i - b)] = inv[radj[i]];
     }
 }

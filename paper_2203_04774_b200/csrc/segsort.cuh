@@ -27,6 +27,12 @@ struct SortLists {
     unsigned int* counts;  // [0] warp, [1] block, [2] big
 };
 
+// Row r is adj[off[r], off[r] + L): L = len[r] when a length array is given
+// (the out-CSR, whose rows are padded to quads), else off[r + 1] - off[r].
+__device__ __forceinline__ uint64_t row_len(const uint64_t* off, const uint32_t* len, uint64_t r) {
+    return len ? static_cast<uint64_t>(len[r]) : off[r + 1] - off[r];
+}
+
 constexpr uint32_t kSortThreadMax = 16;
 constexpr uint32_t kSortWarpMax = 256;
 constexpr uint32_t kSortBlockMax = 4096;
@@ -42,7 +48,7 @@ __device__ __forceinline__ void warp_append(uint32_t* list, unsigned int* count,
 }
 
 // Thread per row: sorts rows of length <= 16 in registers, lists the others.
-__global__ void __launch_bounds__(256) k_sort_small(uint32_t n, const uint64_t* __restrict__ off,
+__global__ void __launch_bounds__(256) k_sort_small(uint32_t n, const uint64_t* __restrict__ off, const uint32_t* __restrict__ len,
                                                     uint32_t* __restrict__ adj, SortLists lists) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const uint64_t start = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -53,7 +59,7 @@ __global__ void __launch_bounds__(256) k_sort_small(uint32_t n, const uint64_t* 
         uint64_t b = 0, L = 0;
         if (r < n) {
             b = off[r];
-            L = off[r + 1] - b;
+            L = row_len(off, len, r);
         }
         if (L >= 2 && L <= kSortThreadMax) {
             uint32_t a[kSortThreadMax];
@@ -90,7 +96,7 @@ struct U32Less {
 
 constexpr int kWarpSortItems = kSortWarpMax / 32;
 
-__global__ void __launch_bounds__(256) k_sort_warp(const uint64_t* __restrict__ off, uint32_t* __restrict__ adj,
+__global__ void __launch_bounds__(256) k_sort_warp(const uint64_t* __restrict__ off, const uint32_t* __restrict__ len, uint32_t* __restrict__ adj,
                                                    const uint32_t* __restrict__ rows,
                                                    const unsigned int* __restrict__ count) {
     using WS = cub::WarpMergeSort<uint32_t, kWarpSortItems, 32>;
@@ -100,7 +106,7 @@ __global__ void __launch_bounds__(256) k_sort_warp(const uint64_t* __restrict__ 
     for (unsigned i = blockIdx.x * 8 + warp; i < total; i += gridDim.x * 8) {
         const uint32_t r = rows[i];
         const uint64_t b = off[r];
-        const int L = (int)(off[r + 1] - b);
+        const int L = (int)row_len(off, len, r);
         uint32_t* p = adj + b;
         uint32_t k[kWarpSortItems];
 #pragma unroll
@@ -121,7 +127,7 @@ __global__ void __launch_bounds__(256) k_sort_warp(const uint64_t* __restrict__ 
 constexpr int kBlockSortThreads = 256;
 constexpr int kBlockSortItems = kSortBlockMax / kBlockSortThreads;
 
-__global__ void __launch_bounds__(kBlockSortThreads) k_sort_block(const uint64_t* __restrict__ off,
+__global__ void __launch_bounds__(kBlockSortThreads) k_sort_block(const uint64_t* __restrict__ off, const uint32_t* __restrict__ len,
                                                                   uint32_t* __restrict__ adj,
                                                                   const uint32_t* __restrict__ rows,
                                                                   const unsigned int* __restrict__ count,
@@ -132,7 +138,7 @@ __global__ void __launch_bounds__(kBlockSortThreads) k_sort_block(const uint64_t
     for (unsigned i = blockIdx.x; i < total; i += gridDim.x) {
         const uint32_t r = rows[i];
         const uint64_t b = off[r];
-        const int L = (int)(off[r + 1] - b);
+        const int L = (int)row_len(off, len, r);
         uint32_t* p = adj + b;
         uint32_t k[kBlockSortItems];
         // blocked arrangement; padding (all ones) sorts last under end_bit > bits(n-1)
@@ -167,7 +173,7 @@ struct BigSortSmem {
     } u;
 };
 
-__global__ void __launch_bounds__(kBigThreads) k_sort_big(uint32_t n, const uint64_t* __restrict__ off,
+__global__ void __launch_bounds__(kBigThreads) k_sort_big(uint32_t n, const uint64_t* __restrict__ off, const uint32_t* __restrict__ len,
                                                           uint32_t* __restrict__ adj, uint32_t* __restrict__ tmpbuf,
                                                           const uint32_t* __restrict__ rows,
                                                           const unsigned int* __restrict__ count) {
@@ -182,7 +188,7 @@ __global__ void __launch_bounds__(kBigThreads) k_sort_big(uint32_t n, const uint
     for (unsigned ri = blockIdx.x; ri < total; ri += gridDim.x) {
         const uint32_t r = rows[ri];
         const uint64_t b = off[r];
-        const uint64_t L = off[r + 1] - b;
+        const uint64_t L = row_len(off, len, r);
         uint32_t* p = adj + b;
         uint32_t* t = tmpbuf + b;
         for (uint32_t w = tid; w < H; w += kBigThreads) S.cursor[w] = 0;

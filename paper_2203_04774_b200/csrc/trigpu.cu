@@ -160,32 +160,32 @@ tl_status scan_offsets(tl_ctx* ctx, uint32_t n, const uint32_t* cnt, uint64_t* o
 }
 
 // Segmented sort of every row of (off, adj) in place; tmp has >= off[n] slots.
-tl_status sort_rows(tl_ctx* ctx, uint32_t n, uint64_t* off, uint32_t* adj, uint32_t* tmp) {
+tl_status sort_rows(tl_ctx* ctx, uint32_t n, uint64_t* off, const uint32_t* len, uint32_t* adj, uint32_t* tmp) {
     ENSURE(small, 128);
     auto* counts = static_cast<unsigned int*>(ctx->small.p);
     CK(cudaMemsetAsync(counts, 0, 4 * sizeof(unsigned int), ctx->s));
     uint32_t* lists = P<uint32_t>(ctx->lists);
     SortLists L{lists, lists + n, lists + 2 * (uint64_t)n, counts};
-    k_sort_small<<<grid_for(n, 256, ctx->sms * 16), 256, 0, ctx->s>>>(n, off, adj, L);
+    k_sort_small<<<grid_for(n, 256, ctx->sms * 16), 256, 0, ctx->s>>>(n, off, len, adj, L);
     LAUNCHED();
     unsigned int h[4];
     CK(cudaMemcpyAsync(h, counts, sizeof(h), cudaMemcpyDeviceToHost, ctx->s));
     CK(cudaStreamSynchronize(ctx->s));
     const int end_bit = std::min(32, (int)(32 - __builtin_clz(std::max(n, 2u) - 1)) + 1);
     if (h[0]) {
-        k_sort_warp<<<grid_for((uint64_t)h[0] * 32, 256, ctx->sms * 8), 256, 0, ctx->s>>>(off, adj, L.warp_rows,
+        k_sort_warp<<<grid_for((uint64_t)h[0] * 32, 256, ctx->sms * 8), 256, 0, ctx->s>>>(off, len, adj, L.warp_rows,
                                                                                           counts + 0);
         LAUNCHED();
     }
     if (h[1]) {
         k_sort_block<<<std::min<unsigned>(h[1], ctx->sms * 8), kBlockSortThreads, 0, ctx->s>>>(
-            off, adj, L.block_rows, counts + 1, end_bit);
+            off, len, adj, L.block_rows, counts + 1, end_bit);
         LAUNCHED();
     }
     if (h[2]) {
         const size_t smem = sizeof(BigSortSmem);
         CK(cudaFuncSetAttribute(k_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_sort_big<<<std::min<unsigned>(h[2], ctx->sms * 2), kBigThreads, smem, ctx->s>>>(n, off, adj, tmp,
+        k_sort_big<<<std::min<unsigned>(h[2], ctx->sms * 2), kBigThreads, smem, ctx->s>>>(n, off, len, adj, tmp,
                                                                                        L.big_rows, counts + 2);
         LAUNCHED();
     }
@@ -206,7 +206,6 @@ tl_status orient_core(tl_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* goff,
     ENSURE(outdeg, (size_t)n * 4);
     ENSURE(indeg, (size_t)n * 4);
     ENSURE(out_off, ((size_t)n + 1) * 8);
-    ENSURE(out_adj, m * 4 + 64);  // +16 words: bulk copies round row ends up to 16 B
     ENSURE(lists, (size_t)n * 4 * kClasses);
     ENSURE(small, 128);
     auto* flags = static_cast<unsigned long long*>(ctx->small.p);  // [0] err, [4..] scratch
@@ -232,26 +231,38 @@ tl_status orient_core(tl_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* goff,
         LAUNCHED();
     }
     CK(cudaEventRecord(ctx->ev[PH_RELABEL], ctx->s));
-    unsigned long long errflag = 0;
+    // out rows padded to quads: out_off holds the padded starts (multiples
+    // of 4), outdeg the lengths; the pad slots hold kNone
+    uint32_t* plen = P<uint32_t>(ctx->lists) + 4 * (uint64_t)n;
+    if (n) {
+        k_pad_len<<<grid_for(n, 256, big), 256, 0, ctx->s>>>(n, P<uint32_t>(ctx->outdeg), plen);
+        LAUNCHED();
+    }
+    tl_status st = scan_offsets(ctx, n, plen, P<uint64_t>(ctx->out_off));
+    if (st != TL_OK) return st;
+    CK(cudaEventRecord(ctx->ev[PH_SCAN], ctx->s));
+    unsigned long long errflag = 0, padded = 0;
     CK(cudaMemcpyAsync(&errflag, flags, 8, cudaMemcpyDeviceToHost, ctx->s));
+    CK(cudaMemcpyAsync(&padded, P<uint64_t>(ctx->out_off) + n, 8, cudaMemcpyDeviceToHost, ctx->s));
     CK(cudaStreamSynchronize(ctx->s));
     if (errflag & 3ull) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "orient: ordering does not match graph (rank is not a permutation of [0, n))");
     if (errflag & 4ull) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "orient: adjacency violates the Graph invariants (rows must be strictly increasing, in range, loop-free)");
-
-    tl_status st = scan_offsets(ctx, n, P<uint32_t>(ctx->outdeg), P<uint64_t>(ctx->out_off));
-    if (st != TL_OK) return st;
-    CK(cudaEventRecord(ctx->ev[PH_SCAN], ctx->s));
+    if (padded / 4 >= (1ull << 32)) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "orient: graph too large (> 2^32 quads of out-rows)");
+    ENSURE(out_adj, padded * 4 + 64);
     if (n) {
         k_scatter<<<grid_for((uint64_t)n, 256, big * 2), 256, 0, ctx->s>>>(
-            n, goff, P<uint32_t>(ctx->radj), rank, P<uint64_t>(ctx->out_off), P<uint32_t>(ctx->out_adj));
+            n, goff, P<uint32_t>(ctx->radj), rank, P<uint64_t>(ctx->out_off), P<uint32_t>(ctx->outdeg),
+            P<uint32_t>(ctx->out_adj));
         LAUNCHED();
         k_scatter_long<<<ctx->sms * 2, kLongThreads, 0, ctx->s>>>(goff, P<uint32_t>(ctx->radj), rank,
-                                                                  P<uint64_t>(ctx->out_off), P<uint32_t>(ctx->out_adj),
+                                                                  P<uint64_t>(ctx->out_off), P<uint32_t>(ctx->outdeg),
+                                                                  P<uint32_t>(ctx->out_adj),
                                                                   long_rows, long_cnt, long_cnt + 2);
         LAUNCHED();
     }
     CK(cudaEventRecord(ctx->ev[PH_SCATTER], ctx->s));
-    st = sort_rows(ctx, n, P<uint64_t>(ctx->out_off), P<uint32_t>(ctx->out_adj), P<uint32_t>(ctx->radj));
+    st = sort_rows(ctx, n, P<uint64_t>(ctx->out_off), P<uint32_t>(ctx->outdeg), P<uint32_t>(ctx->out_adj),
+                   P<uint32_t>(ctx->radj));
     if (st != TL_OK) return st;
     CK(cudaEventRecord(ctx->ev[PH_SORT], ctx->s));
     // costs + max out-degree
@@ -282,12 +293,13 @@ tl_status orient_core(tl_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* goff,
 }
 
 // k_transpose: in-row s receives r for every successor s of r.
-__global__ void k_transpose(uint32_t n, const uint64_t* __restrict__ out_off, const uint32_t* __restrict__ out_adj,
-                            unsigned long long* __restrict__ cursor, uint32_t* __restrict__ in_adj) {
+__global__ void k_transpose(uint32_t n, const uint64_t* __restrict__ out_off, const uint32_t* __restrict__ outdeg,
+                            const uint32_t* __restrict__ out_adj, unsigned long long* __restrict__ cursor,
+                            uint32_t* __restrict__ in_adj) {
     const unsigned lane = lane_id();
     const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t r = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; r < n; r += warps) {
-        const uint64_t b = out_off[r], e = out_off[r + 1];
+        const uint64_t b = out_off[r], e = b + outdeg[r];
         for (uint64_t i = b + lane; i < e; i += 32) {
             const uint32_t s = out_adj[i];
             in_adj[atomicAdd(&cursor[s], 1ull)] = static_cast<uint32_t>(r);
@@ -313,10 +325,11 @@ tl_status ensure_in_csr(tl_ctx* ctx) {
     if (n) {
         CK(cudaMemcpyAsync(cursor, ctx->in_off.p, (size_t)n * 8, cudaMemcpyDeviceToDevice, ctx->s));
         k_transpose<<<grid_for((uint64_t)n * 32, 256, ctx->sms * 32), 256, 0, ctx->s>>>(
-            n, P<uint64_t>(ctx->out_off), P<uint32_t>(ctx->out_adj), cursor, P<uint32_t>(ctx->in_adj));
+            n, P<uint64_t>(ctx->out_off), P<uint32_t>(ctx->outdeg), P<uint32_t>(ctx->out_adj), cursor,
+            P<uint32_t>(ctx->in_adj));
         LAUNCHED();
     }
-    st = sort_rows(ctx, n, P<uint64_t>(ctx->in_off), P<uint32_t>(ctx->in_adj), P<uint32_t>(ctx->radj));
+    st = sort_rows(ctx, n, P<uint64_t>(ctx->in_off), nullptr, P<uint32_t>(ctx->in_adj), P<uint32_t>(ctx->radj));
     if (st != TL_OK) return st;
     CK(cudaEventRecord(ctx->ev[PH_COUNT + 1], ctx->s));
     CK(cudaStreamSynchronize(ctx->s));
@@ -578,14 +591,16 @@ TL_API tl_status tl_list(tl_ctx* ctx, int algo, unsigned out_flags, tl_stats* ou
     ListParams base{};
     base.n = n;
     base.set_off = algo == TL_ALGO_APM ? P<uint64_t>(ctx->out_off) : P<uint64_t>(ctx->in_off);
+    base.set_len = algo == TL_ALGO_APM ? P<uint32_t>(ctx->outdeg) : P<uint32_t>(ctx->indeg);
     base.set_adj = algo == TL_ALGO_APM ? P<uint32_t>(ctx->out_adj) : P<uint32_t>(ctx->in_adj);
     base.out_off = P<uint64_t>(ctx->out_off);
+    base.out_len = P<uint32_t>(ctx->outdeg);
     base.out_adj = P<uint32_t>(ctx->out_adj);
     base.inv = P<uint32_t>(ctx->inv);
     if ((out_flags & TL_OUT_CHECKSUM) && !ctx->hv_built) {
         // checksum sink: h(dense id) per rank, once per orientation
-        ENSURE(hv, (size_t)std::max<uint32_t>(n, 1) * 8);
-        if (n) {
+        ENSURE(hv, ((size_t)n + 1) * 8);
+        {
             k_vertex_hash<<<grid_for(n, 256, ctx->sms * 16), 256, 0, ctx->s>>>(n, P<uint32_t>(ctx->inv),
                                                                               P<unsigned long long>(ctx->hv));
             LAUNCHED();
@@ -604,7 +619,7 @@ TL_API tl_status tl_list(tl_ctx* ctx, int algo, unsigned out_flags, tl_stats* ou
     uint32_t* const lists[kClasses] = {L, L + n, L + 2 * (uint64_t)n, L + 3 * (uint64_t)n, L + 4 * (uint64_t)n};
     SeedLists SL{{lists[0], lists[1], lists[2], lists[3], lists[4]}, counts};
     if (n) {
-        k_classify_seeds<<<grid_for(n, 256, ctx->sms * 16), 256, 0, ctx->s>>>(n, base.set_off, SL);
+        k_classify_seeds<<<grid_for(n, 256, ctx->sms * 16), 256, 0, ctx->s>>>(n, base.set_len, SL);
         LAUNCHED();
     }
     CK(cudaEventRecord(ctx->ev[PH_CLASSIFY], ctx->s));
@@ -732,7 +747,7 @@ TL_API tl_status tl_fetch_oriented(tl_ctx* ctx, uint64_t* succ_off, uint32_t* su
         }
         if (n) {
             k_export_rows<<<grid_for((uint64_t)n * 32, 256, ctx->sms * 32), 256, 0, ctx->s>>>(
-                n, P<uint32_t>(ctx->rank), P<uint32_t>(ctx->inv), roff, radj, P<uint64_t>(doff), P<uint32_t>(dadj));
+                n, P<uint32_t>(ctx->rank), P<uint32_t>(ctx->inv), roff, deg, radj, P<uint64_t>(doff), P<uint32_t>(dadj));
             ++ctx->launches;
         }
         cudaError_t e = cudaGetLastError();
