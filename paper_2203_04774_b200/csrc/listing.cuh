@@ -220,7 +220,8 @@ struct Sink {
     static constexpr bool kFastSum = (F & F_CHECKSUM) != 0u && (F & (F_VCOUNT | F_LIST)) == 0u;
     static constexpr bool kBuffered = (F & (F_VCOUNT | F_LIST)) != 0u;
     unsigned long long cnt = 0, sum = 0;
-    unsigned long long hs = 0;  // h(seed)
+    unsigned long long hs = 0;    // h(seed)
+    unsigned long long acc = 0;   // this seed's sum of h(x) h(y); times h(s) at end_unit
     unsigned seed_hits = 0;
     unsigned buf = 0;      // shared address of this warp's kHitBuf uint2 entries
     unsigned pending = 0;  // warp-uniform
@@ -232,7 +233,7 @@ struct Sink {
     // One hit with its own x (short-row stream), kFastSum only.
     __device__ __forceinline__ void direct(const ListParams& P, bool hit, uint32_t x, uint32_t y) {
         if constexpr (kFastSum)
-            if (hit) sum += hs * __ldg(P.hv + x) * __ldg(P.hv + y);
+            if (hit) acc += __ldg(P.hv + x) * __ldg(P.hv + y);
     }
 
     // One 32-wide batch of hits (called convergently by the warp), kBuffered only.
@@ -259,7 +260,7 @@ struct Sink {
             }
         }
         if constexpr ((F & F_CHECKSUM) != 0u)
-            if (hit) sum += hs * __ldg(P.hv + x) * __ldg(P.hv + y);
+            if (hit) acc += __ldg(P.hv + x) * __ldg(P.hv + y);
         if constexpr ((F & F_LIST) != 0u) {
             const uint32_t ru = ALGO == ALGO_APM ? seed : x;
             const uint32_t rv = ALGO == ALGO_APM ? x : y;
@@ -307,6 +308,10 @@ struct Sink {
             const unsigned long long h = warp_sum64(seed_hits);
             if (lane_id() == 0 && h) atomicAdd(&P.vcount[seed], h);
             seed_hits = 0;
+        }
+        if constexpr ((F & F_CHECKSUM) != 0u) {
+            sum += hs * acc;
+            acc = 0;
         }
     }
 
@@ -410,19 +415,24 @@ __device__ __forceinline__ void stream_quads(const ListParams& P, uint32_t seed,
             // h(s) h(x). Straight-line predicated gathers (hub ranks: L1/L2
             // hits), all in flight before the first use.
             if (__any_sync(FULL, hm != 0)) {
-                const unsigned long long* const hv = P.hv;
+                // hv base held in a register (else it is re-read from the
+                // constant bank per predicated load); lanes without a hit
+                // read hv[n] = 0, so the loads need no predicate
+                const unsigned long long* hv;
+                asm("mov.b64 %0, %1;" : "=l"(hv) : "l"(P.hv));
+                const uint32_t zero = P.n;
                 unsigned long long sy[QU];
 #pragma unroll
                 for (int i = 0; i < QU; ++i) {
-                    const unsigned long long a0 = (hb[i] & 1u) ? __ldg(hv + y[i].x) : 0ull;
-                    const unsigned long long a1 = (hb[i] & 2u) ? __ldg(hv + y[i].y) : 0ull;
-                    const unsigned long long a2 = (hb[i] & 4u) ? __ldg(hv + y[i].z) : 0ull;
-                    const unsigned long long a3 = (hb[i] & 8u) ? __ldg(hv + y[i].w) : 0ull;
+                    const unsigned long long a0 = __ldg(hv + ((hb[i] & 1u) ? y[i].x : zero));
+                    const unsigned long long a1 = __ldg(hv + ((hb[i] & 2u) ? y[i].y : zero));
+                    const unsigned long long a2 = __ldg(hv + ((hb[i] & 4u) ? y[i].z : zero));
+                    const unsigned long long a3 = __ldg(hv + ((hb[i] & 8u) ? y[i].w : zero));
                     sy[i] = (a0 + a1) + (a2 + a3);
                 }
 #pragma unroll
                 for (int i = 0; i < QU; ++i)
-                    if (hb[i]) sink.sum += sy[i] * (sink.hs * __ldg(hv + ch[i].x));
+                    if (hb[i]) sink.acc += sy[i] * __ldg(hv + ch[i].x);
             }
         }
     }
@@ -643,9 +653,15 @@ __device__ __forceinline__ void attach_scratch(Sink<ALGO, F>& sink, unsigned cha
     sink.buf = smem_addr(base + (threadIdx.x >> 5) * kHitBuf * 8);
 }
 
+// CTAs per SM of the warp-class kernels: 4 (64 registers) for count only; the
+// sinks need more registers (3 CTAs, 80 registers) or they spill in the hot loop
 #ifndef TRIGPU_WARP_MINB
 #define TRIGPU_WARP_MINB 4
 #endif
+#ifndef TRIGPU_WARP_MINB_SINK
+#define TRIGPU_WARP_MINB_SINK 3
+#endif
+#define WARP_MINB(F) ((F) == 0u ? TRIGPU_WARP_MINB : TRIGPU_WARP_MINB_SINK)
 
 // ---- class R: |S| <= 32, warp per seed --------------------------------------
 constexpr int kRWarps = 8;
@@ -692,7 +708,7 @@ constexpr uint32_t kHBitsA = 15, kHBitsB = 13;  // 4 KB window + 1 KB region B p
 constexpr size_t kHBmBytes = win_bytes(kHBitsA, kHBitsB);
 
 template <int ALGO, unsigned F>
-__global__ void __launch_bounds__(kHWarps * 32, TRIGPU_WARP_MINB) k_list_warp(ListParams P) {
+__global__ void __launch_bounds__(kHWarps * 32, WARP_MINB(F)) k_list_warp(ListParams P) {
     extern __shared__ __align__(16) unsigned char dsm[];
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
     uint32_t* bma = reinterpret_cast<uint32_t*>(dsm + warp_scratch_bytes<F>(kHWarps) + warp * kHBmBytes);
