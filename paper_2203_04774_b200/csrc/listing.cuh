@@ -374,14 +374,15 @@ __device__ __forceinline__ void stream_quads(const ListParams& P, uint32_t seed,
         for (int i = 0; i < QU; ++i) {
             hb[i] = probe.bit(y[i].x) | (probe.bit(y[i].y) << 1) | (probe.bit(y[i].z) << 2) | (probe.bit(y[i].w) << 3);
             hb[i] = pr[i] ? hb[i] : 0u;
-            if constexpr (Probe::low)
-                any |= pr[i] && (probe.below(y[i].x) | probe.below(y[i].y) | probe.below(y[i].z) | probe.below(y[i].w));
+            // a quad's first element is its smallest (rows sorted, pads last)
+            if constexpr (Probe::low) any |= pr[i] && probe.below(y[i].x);
         }
         if constexpr (Probe::low) {
             // elements below the window: region-B candidates, verified here
             if (__any_sync(FULL, any)) {
 #pragma unroll
                 for (int i = 0; i < QU; ++i) {
+                    if (!__any_sync(FULL, pr[i] && probe.below(y[i].x))) continue;
                     const uint32_t e[4] = {y[i].x, y[i].y, y[i].z, y[i].w};
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
@@ -704,7 +705,10 @@ __global__ void __launch_bounds__(kRWarps * 32, TRIGPU_WARP_MINB) k_list_reg(Lis
 
 // ---- class H: 32 < |S| <= 256, warp per seed --------------------------------
 constexpr int kHWarps = 8;
-constexpr uint32_t kHBitsA = 15, kHBitsB = 13;  // 4 KB window + 1 KB region B per warp
+#ifndef TRIGPU_H_BITS_A
+#define TRIGPU_H_BITS_A 16
+#endif
+constexpr uint32_t kHBitsA = TRIGPU_H_BITS_A, kHBitsB = 13;  // 8 KB window + 1 KB region B per warp
 constexpr size_t kHBmBytes = win_bytes(kHBitsA, kHBitsB);
 
 template <int ALGO, unsigned F>
