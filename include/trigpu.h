@@ -92,6 +92,23 @@ TL_API tl_status tl_orient(tl_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* 
  * call (inputs already resident in HBM). */
 TL_API tl_status tl_orient_device(tl_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* d_offsets,
                                   const uint32_t* d_adj, const uint32_t* d_rank);
+/* Orderings on the device: the reference's degree order
+ * (ordering.cpp:66-96: counting sort by degree, ascending, ties by ascending
+ * id) and split order (ordering.cpp:98-109: degree-descending sequence, even
+ * positions fill the front, odd the back), bit-identical to the reference's
+ * (tests/test_gpu_parity.py). degree(v) = offsets[v + 1] - offsets[v] of the
+ * Graph CSR. tl_order: host arrays in and out; tl_order_device: device
+ * arrays. Replaces degree_order / split_order (ordering.hpp) on the listing
+ * path; the other orderings stay the reference's host code. */
+enum { TL_ORDER_DEGREE = 0, TL_ORDER_SPLIT = 1 };
+TL_API tl_status tl_order(tl_ctx* ctx, uint32_t n, const uint64_t* offsets, int method, uint32_t* rank);
+TL_API tl_status tl_order_device(tl_ctx* ctx, uint32_t n, const uint64_t* d_offsets, int method, uint32_t* d_rank);
+/* tl_orient with the ordering computed on the device by `method`
+ * (TL_ORDER_DEGREE / TL_ORDER_SPLIT): the whole path from the host Graph CSR,
+ * no host ordering. The ranks can be read back with tl_fetch_ranks. */
+TL_API tl_status tl_orient_ordered(tl_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* offsets,
+                                   const uint32_t* adj, int method);
+TL_API tl_status tl_fetch_ranks(tl_ctx* ctx, uint32_t* rank);
 /* Mismatched sizes (rank length != n) are reported as in oriented_view.cpp:8-9. */
 TL_API tl_status tl_check_sizes(uint32_t graph_n, uint32_t rank_n);
 

@@ -29,6 +29,8 @@ TL_ERR_STATE = 4
 TL_ERR_CAPACITY = 5
 TL_ALGO_APP = 0
 TL_ALGO_APM = 1
+TL_ORDER_DEGREE = 0
+TL_ORDER_SPLIT = 1
 TL_OUT_COUNT = 0
 TL_OUT_CHECKSUM = 1
 TL_OUT_VERTEX_COUNTS = 2
@@ -40,7 +42,8 @@ TRIGPU_SYMBOLS = (
     "tl_orient_device", "tl_check_sizes", "tl_list", "tl_fetch_triangles",
     "tl_fetch_vertex_counts", "tl_fetch_oriented", "tl_cost_report",
     "tl_host_register", "tl_host_unregister", "tl_phase_times", "tl_phase_name",
-    "tl_timer_start", "tl_timer_stop",
+    "tl_timer_start", "tl_timer_stop", "tl_order", "tl_order_device", "tl_orient_ordered",
+    "tl_fetch_ranks",
 )
 
 
@@ -119,6 +122,14 @@ def trigpu() -> C.CDLL:
     lib.tl_timer_stop.restype = C.c_int
     lib.tl_phase_times.argtypes = [_vp, C.POINTER(C.c_double), C.c_int]
     lib.tl_phase_times.restype = C.c_int
+    lib.tl_order.argtypes = [_vp, _u32, _vp, C.c_int, _vp]
+    lib.tl_order.restype = C.c_int
+    lib.tl_order_device.argtypes = [_vp, _u32, _vp, C.c_int, _vp]
+    lib.tl_order_device.restype = C.c_int
+    lib.tl_orient_ordered.argtypes = [_vp, _u32, _u64, _vp, _vp, C.c_int]
+    lib.tl_orient_ordered.restype = C.c_int
+    lib.tl_fetch_ranks.argtypes = [_vp, _vp]
+    lib.tl_fetch_ranks.restype = C.c_int
     lib.tl_phase_name.argtypes = [C.c_int]
     lib.tl_phase_name.restype = C.c_char_p
     return lib

@@ -253,11 +253,13 @@ struct Sink {
         const uint2 e = hit ? lds64(from + 8u * lane) : make_uint2(0, 0);
         const uint32_t x = e.x, y = e.y;
         if constexpr ((F & F_VCOUNT) != 0u) {
-            if (hit) {
-                atomicAdd(&P.vcount[x], 1ull);
-                atomicAdd(&P.vcount[y], 1ull);
-                ++seed_hits;
-            }
+            // hubs recur within the 32 entries (same x for a chunk's hits,
+            // the same hub y for many x): one atomic per distinct vertex
+            const unsigned gx = __match_any_sync(FULL, hit ? x : kNone);
+            const unsigned gy = __match_any_sync(FULL, hit ? y : kNone);
+            if (hit && (gx & lanemask_lt()) == 0) atomicAdd(&P.vcount[x], (unsigned long long)__popc(gx));
+            if (hit && (gy & lanemask_lt()) == 0) atomicAdd(&P.vcount[y], (unsigned long long)__popc(gy));
+            seed_hits += hit;
         }
         if constexpr ((F & F_CHECKSUM) != 0u)
             if (hit) acc += __ldg(P.hv + x) * __ldg(P.hv + y);

@@ -427,6 +427,32 @@ __global__ void __launch_bounds__(256) k_cost(uint32_t n, const uint32_t* __rest
 }
 
 // max over rows of the out-degree (listing batch arithmetic is 32-bit).
+// ---- device orderings (ordering.cpp:66-109) ----------------------------------
+// Sort keys of the reference's bucket sort: degree ascending (degree order)
+// or descending via ~degree (split order); the values are the vertex ids in
+// ascending order and the radix sort is stable, so ties keep ascending ids,
+// exactly as the reference's counting sort fills each degree bucket.
+__global__ void k_degree_keys(uint32_t n, const uint64_t* __restrict__ off, bool desc, uint32_t* __restrict__ key,
+                              uint32_t* __restrict__ val) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += stride) {
+        const uint32_t d = static_cast<uint32_t>(off[v + 1] - off[v]);
+        key[v] = desc ? ~d : d;
+        val[v] = static_cast<uint32_t>(v);
+    }
+}
+
+// Position p of the sorted sequence -> rank. Split: ordering.cpp:103-106
+// (0-based parity formula).
+__global__ void k_rank_from_sequence(uint32_t n, const uint32_t* __restrict__ seq, bool split,
+                                     uint32_t* __restrict__ rank) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n; p += stride) {
+        const uint32_t pp = static_cast<uint32_t>(p);
+        rank[seq[p]] = !split ? pp : ((pp & 1u) == 0 ? pp / 2 : n - 1 - pp / 2);
+    }
+}
+
 // Padded out-row lengths: rows start on 16-byte boundaries (quads) so the
 // listing reads them as whole quads; pad slots hold kNone.
 __global__ void k_pad_len(uint32_t n, const uint32_t* __restrict__ deg, uint32_t* __restrict__ plen) {

@@ -24,6 +24,8 @@
 
 #include "common.cuh"
 #include "listing.cuh"
+
+#include <cub/device/device_radix_sort.cuh>
 #include "orient.cuh"
 #include "segsort.cuh"
 #include "trigpu.h"
@@ -74,7 +76,7 @@ struct tl_ctx {
     unsigned long long cost[4] = {0, 0, 0, 0};
     double h2d_ms = 0, orient_ms = 0;
 
-    DevBuf goff, gadj, rank, inv, hv, radj, out_off, out_adj, in_off, in_adj, outdeg, indeg, lists, acc,
+    DevBuf goff, gadj, rank, inv, hv, sort_tmp, radj, out_off, out_adj, in_off, in_adj, outdeg, indeg, lists, acc,
         vcount, tri, scan_part, bitmaps, small;
     bool have_vcounts = false, have_tri = false;
     int variant = 0;         // probe flavour (TRIGPU_VARIANT), for A/B measurement
@@ -498,7 +500,8 @@ TL_API void tl_destroy(tl_ctx* ctx) {
     cudaStreamSynchronize(ctx->s2);
     DevBuf* bufs[] = {&ctx->goff,   &ctx->gadj,   &ctx->rank,  &ctx->inv,    &ctx->radj,      &ctx->out_off,
                       &ctx->out_adj, &ctx->in_off, &ctx->in_adj, &ctx->outdeg, &ctx->indeg,     &ctx->lists,
-                      &ctx->acc,    &ctx->vcount, &ctx->tri,   &ctx->scan_part, &ctx->bitmaps, &ctx->small};
+                      &ctx->acc,    &ctx->vcount, &ctx->tri,   &ctx->scan_part, &ctx->bitmaps, &ctx->small,
+                      &ctx->hv,     &ctx->sort_tmp};
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     for (auto& ev : ctx->ev) cudaEventDestroy(ev);
@@ -548,6 +551,86 @@ TL_API tl_status tl_orient(tl_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* 
     st = orient_core(ctx, n, m, P<uint64_t>(ctx->goff), P<uint32_t>(ctx->gadj), P<uint32_t>(ctx->rank));
     if (st != TL_OK) return st;
     ctx->h2d_ms = ctx->phase_ms[PH_H2D] = ev_ms(ctx->ev[PH_COUNT + 2], ctx->ev[PH_H2D]);
+    return TL_OK;
+}
+
+// Degree / split order on the device into d_rank (device, n entries).
+static tl_status order_core(tl_ctx* ctx, uint32_t n, const uint64_t* d_off, int method, uint32_t* d_rank) {
+    if (method != TL_ORDER_DEGREE && method != TL_ORDER_SPLIT)
+        return ctx->fail(TL_ERR_INVALID_ARGUMENT, "order: method must be TL_ORDER_DEGREE or TL_ORDER_SPLIT");
+    if (!n) return TL_OK;
+    // keys / values in and out: 4 x n words of `lists` (free outside tl_list)
+    ENSURE(lists, (size_t)n * 4 * kClasses);
+    uint32_t* L = P<uint32_t>(ctx->lists);
+    uint32_t *k_in = L, *v_in = L + n, *k_out = L + 2 * (uint64_t)n, *v_out = L + 3 * (uint64_t)n;
+    k_degree_keys<<<grid_for(n, 256, ctx->sms * 16), 256, 0, ctx->s>>>(n, d_off, method == TL_ORDER_SPLIT, k_in,
+                                                                        v_in);
+    LAUNCHED();
+    size_t tmp_bytes = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k_in, k_out, v_in, v_out, (int)n, 0, 32, ctx->s));
+    ENSURE(sort_tmp, tmp_bytes + 16);
+    CK(cub::DeviceRadixSort::SortPairs(ctx->sort_tmp.p, tmp_bytes, k_in, k_out, v_in, v_out, (int)n, 0, 32, ctx->s));
+    ctx->launches += 8;  // cub's onesweep passes (histogram + 4 x scan/sweep), approximate
+    k_rank_from_sequence<<<grid_for(n, 256, ctx->sms * 16), 256, 0, ctx->s>>>(n, v_out, method == TL_ORDER_SPLIT,
+                                                                               d_rank);
+    LAUNCHED();
+    return TL_OK;
+}
+
+TL_API tl_status tl_order_device(tl_ctx* ctx, uint32_t n, const uint64_t* d_offsets, int method, uint32_t* d_rank) {
+    if (!ctx || (n && (!d_offsets || !d_rank))) return TL_ERR_INVALID_ARGUMENT;
+    if (n == 0xFFFFFFFFu) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "order: n must be < 2^32 - 1");
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return ctx->cuda_fail("cudaSetDevice", cudaGetLastError());
+    tl_status st = order_core(ctx, n, d_offsets, method, d_rank);
+    if (st != TL_OK) return st;
+    CK(cudaStreamSynchronize(ctx->s));
+    return TL_OK;
+}
+
+TL_API tl_status tl_order(tl_ctx* ctx, uint32_t n, const uint64_t* offsets, int method, uint32_t* rank) {
+    if (!ctx || (n && (!offsets || !rank))) return TL_ERR_INVALID_ARGUMENT;
+    if (n == 0xFFFFFFFFu) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "order: n must be < 2^32 - 1");
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return ctx->cuda_fail("cudaSetDevice", cudaGetLastError());
+    ENSURE(goff, ((size_t)n + 1) * 8);
+    ENSURE(rank, (size_t)n * 4 + 4);
+    CK(cudaMemcpyAsync(ctx->goff.p, offsets, ((size_t)n + 1) * 8, cudaMemcpyHostToDevice, ctx->s));
+    tl_status st = order_core(ctx, n, P<uint64_t>(ctx->goff), method, P<uint32_t>(ctx->rank));
+    if (st != TL_OK) return st;
+    if (n) CK(cudaMemcpyAsync(rank, ctx->rank.p, (size_t)n * 4, cudaMemcpyDeviceToHost, ctx->s));
+    CK(cudaStreamSynchronize(ctx->s));
+    ctx->oriented = false;  // the owned rank / offsets copies were overwritten
+    return TL_OK;
+}
+
+TL_API tl_status tl_orient_ordered(tl_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* offsets, const uint32_t* adj,
+                                   int method) {
+    if (!ctx || (n && !offsets) || (m && !adj)) return TL_ERR_INVALID_ARGUMENT;
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return ctx->cuda_fail("cudaSetDevice", cudaGetLastError());
+    if (n == 0xFFFFFFFFu) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "orient: n must be < 2^32 - 1 (VertexId, common.hpp:11-13)");
+    if (n && offsets[0] != 0) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "orient: offsets[0] must be 0");
+    if (n && offsets[n] != 2 * m) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "orient: offsets[n] must equal 2m");
+    ENSURE(goff, ((size_t)n + 1) * 8);
+    ENSURE(gadj, 2 * m * 4);
+    ENSURE(rank, (size_t)n * 4 + 4);
+    CK(cudaEventRecord(ctx->ev[PH_COUNT + 2], ctx->s));
+    CK(cudaMemcpyAsync(ctx->goff.p, offsets, ((size_t)n + 1) * 8, cudaMemcpyHostToDevice, ctx->s));
+    if (m) CK(cudaMemcpyAsync(ctx->gadj.p, adj, 2 * m * 4, cudaMemcpyHostToDevice, ctx->s));
+    tl_status st = order_core(ctx, n, P<uint64_t>(ctx->goff), method, P<uint32_t>(ctx->rank));
+    if (st != TL_OK) return st;
+    CK(cudaEventRecord(ctx->ev[PH_H2D], ctx->s));
+    st = orient_core(ctx, n, m, P<uint64_t>(ctx->goff), P<uint32_t>(ctx->gadj), P<uint32_t>(ctx->rank));
+    if (st != TL_OK) return st;
+    ctx->h2d_ms = ctx->phase_ms[PH_H2D] = ev_ms(ctx->ev[PH_COUNT + 2], ctx->ev[PH_H2D]);
+    return TL_OK;
+}
+
+TL_API tl_status tl_fetch_ranks(tl_ctx* ctx, uint32_t* rank) {
+    if (!ctx) return TL_ERR_INVALID_ARGUMENT;
+    if (!ctx->oriented) return ctx->fail(TL_ERR_STATE, "tl_fetch_ranks: no oriented view");
+    if (ctx->n && !rank) return TL_ERR_INVALID_ARGUMENT;
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return ctx->cuda_fail("cudaSetDevice", cudaGetLastError());
+    if (ctx->n) CK(cudaMemcpyAsync(rank, ctx->rank.p, (size_t)ctx->n * 4, cudaMemcpyDeviceToHost, ctx->s));
+    CK(cudaStreamSynchronize(ctx->s));
     return TL_OK;
 }
 

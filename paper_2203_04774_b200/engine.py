@@ -93,6 +93,38 @@ class Context:
     def orient_device(self, n: int, m: int, d_offsets: int, d_adj: int, d_rank: int) -> None:
         _check(self._p, _native.trigpu().tl_orient_device(self._p, n, m, d_offsets, d_adj, d_rank))
 
+    # device orderings (degree_order / split_order, ordering.cpp:66-109)
+    _ORDERS = {"degree": _native.TL_ORDER_DEGREE, "split": _native.TL_ORDER_SPLIT}
+
+    def order(self, offsets: np.ndarray, method: str) -> np.ndarray:
+        """Ordering::ranks() of degree_order / split_order, computed on the GPU."""
+        if method not in self._ORDERS:
+            raise ValueError(f"order: device orderings are {sorted(self._ORDERS)}")
+        offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+        n = offsets.shape[0] - 1
+        rank = np.empty(max(n, 1), dtype=np.uint32)
+        _check(self._p, _native.trigpu().tl_order(self._p, n, offsets.ctypes.data, self._ORDERS[method],
+                                                  rank.ctypes.data))
+        return rank[:n]
+
+    def order_device(self, n: int, d_offsets: int, method: str, d_rank: int) -> None:
+        _check(self._p, _native.trigpu().tl_order_device(self._p, n, d_offsets, self._ORDERS[method], d_rank))
+
+    def orient_ordered(self, offsets: np.ndarray, adj: np.ndarray, method: str) -> None:
+        """tl_orient with the ordering computed on the device (no host ordering)."""
+        if method not in self._ORDERS:
+            raise ValueError(f"orient_ordered: device orderings are {sorted(self._ORDERS)}")
+        offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+        adj = np.ascontiguousarray(adj, dtype=np.uint32)
+        _check(self._p, _native.trigpu().tl_orient_ordered(self._p, offsets.shape[0] - 1, adj.shape[0] // 2,
+                                                           offsets.ctypes.data, adj.ctypes.data,
+                                                           self._ORDERS[method]))
+
+    def fetch_ranks(self, n: int) -> np.ndarray:
+        rank = np.empty(max(n, 1), dtype=np.uint32)
+        _check(self._p, _native.trigpu().tl_fetch_ranks(self._p, rank.ctypes.data))
+        return rank[:n]
+
     def list(self, algo: int, flags: int) -> TlStats:
         st = TlStats()
         _check(self._p, _native.trigpu().tl_list(self._p, algo, flags, C.byref(st)))

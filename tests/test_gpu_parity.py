@@ -290,3 +290,32 @@ def test_probe_filter_path(monkeypatch, shrink):
                 assert canon(c.fetch_triangles()).tolist() == ent[an]["canonical"]
     finally:
         c.close()
+
+
+@pytest.mark.parametrize("meth", ["degree", "split"])
+def test_device_orderings_match_reference(meth):
+    """tl_order (degree / split on the GPU) is bit-identical to the
+    reference's degree_order / split_order (ordering.cpp:66-109), including
+    the tie-breaks, and tl_orient_ordered lists the same triangles."""
+    c = tg.Context(0)
+    try:
+        graphs = [tg.gen_gnm(0, 0, 1), tg.gen_gnm(1, 0, 1), tg.gen_gnm(60, 400, 11), tg.gen_rmat(14, 16, 2),
+                  tg.gen_chung_lu(30000, 400000, seed=3), tg.gen_ws(20000, 16, 0.1, seed=5)]
+        for case in cases():
+            off, adj = case_csr(case)
+            graphs.append(host.Graph(off, adj))
+        for g in graphs:
+            pi, _ = host.compute_order(g, meth)
+            assert np.array_equal(c.order(g.offsets, meth), pi.ranks)
+            if g.n == 0:
+                continue
+            c.orient_ordered(g.offsets, g.adjacency, meth)
+            assert np.array_equal(c.fetch_ranks(g.n), pi.ranks)
+            st = c.list(TL_ALGO_APM, TL_OUT_CHECKSUM)
+            view = oracle.orient(g.offsets, g.adjacency, pi.ranks)
+            exp = oracle.list_triangles(view, TL_ALGO_APM, threads=8)
+            assert (st.triangle_count, st.checksum) == (exp.triangle_count, exp.checksum)
+        with pytest.raises(ValueError):
+            c.order(graphs[2].offsets, "core")
+    finally:
+        c.close()
