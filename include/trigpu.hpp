@@ -73,6 +73,23 @@ inline Context& default_context() {
     return ctx;
 }
 
+// degree_order / split_order (ordering.cpp:66-109) computed on the GPU;
+// returns the reference's Ordering type with bit-identical ranks.
+inline trilist::Ordering device_order(const trilist::Graph& g, int method, Context& ctx = default_context()) {
+    const VertexId n = g.vertex_count();
+    std::vector<std::uint64_t> off(static_cast<std::size_t>(n) + 1, 0);
+    for (VertexId u = 0; u < n; ++u) off[u + 1] = off[u] + g.degree(u);
+    std::vector<VertexId> rank(n);
+    ctx.check(tl_order(ctx.get(), n, off.data(), method, rank.data()));
+    return trilist::Ordering::from_ranks(std::move(rank));
+}
+inline trilist::Ordering degree_order(const trilist::Graph& g, Context& ctx = default_context()) {
+    return device_order(g, TL_ORDER_DEGREE, ctx);
+}
+inline trilist::Ordering split_order(const trilist::Graph& g, Context& ctx = default_context()) {
+    return device_order(g, TL_ORDER_SPLIT, ctx);
+}
+
 // GPU-resident OrientedView (oriented_view.hpp:17-50). The device holds one
 // view per Context; constructing another view in the same context replaces it
 // (each listing call re-orients if needed).

@@ -826,7 +826,8 @@ __global__ void __launch_bounds__(CFG::kThreads, CFG::kMinBlocks) k_list_cta(Lis
         __syncthreads();
         const uint32_t nchunks = total_chunks;
         with_win_probe(P, smem_addr(bma), smem_addr(bmb), g, RowVerify{row, d}, [&](const auto& probe) {
-            // equal, contiguous share of the seed's chunks per warp
+            // equal, contiguous share of the seed's chunks per warp (measured
+            // faster than claiming runs of 8 chunks from a shared counter)
             const unsigned warp = threadIdx.x >> 5;
             const uint32_t gb = static_cast<uint32_t>((static_cast<uint64_t>(nchunks) * warp) / CFG::kWarps);
             const uint32_t ge = static_cast<uint32_t>((static_cast<uint64_t>(nchunks) * (warp + 1)) / CFG::kWarps);

@@ -182,6 +182,22 @@ int main() {
     }
     section("orient partitions each neighborhood (graph_test.cpp:145-181)", f0);
 
+    f0 = g_fail;  // device orderings == the reference's (ordering.cpp:66-109)
+    {
+        for (std::uint64_t seed = 0; seed < 40; ++seed) {
+            const Graph g = random_small_graph(seed, 60, 400);
+            expect(trigpu::degree_order(g).ranks().size() == g.vertex_count(), "degree order size");
+            const auto a = trigpu::degree_order(g), b = degree_order(g);
+            const auto c = trigpu::split_order(g), d = split_order(g);
+            expect(std::equal(a.ranks().begin(), a.ranks().end(), b.ranks().begin()), "device degree order");
+            expect(std::equal(c.ranks().begin(), c.ranks().end(), d.ranks().begin()), "device split order");
+        }
+        const Graph g = gen_gnm(100000, 1000000, 4242);
+        const auto a = trigpu::degree_order(g), b = degree_order(g);
+        expect(std::equal(a.ranks().begin(), a.ranks().end(), b.ranks().begin()), "device degree order, C1");
+    }
+    section("device degree / split orderings (ordering.cpp:66-109)", f0);
+
     f0 = g_fail;  // acceptance criteria 1-3
     {
         const int c0 = g_fail;
