@@ -109,6 +109,18 @@ TL_API tl_status tl_order_device(tl_ctx* ctx, uint32_t n, const uint64_t* d_offs
 TL_API tl_status tl_orient_ordered(tl_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* offsets,
                                    const uint32_t* adj, int method);
 TL_API tl_status tl_fetch_ranks(tl_ctx* ctx, uint32_t* rank);
+
+/* Raw labeled edge list -> the reference's Graph CSR, on the device
+ * (SURVEY §8f): normalize (graph.cpp:115-151: loops dropped, endpoints
+ * canonicalised, duplicates merged, labels = sorted distinct endpoints,
+ * dense id = label rank) + Graph::from_dense_edges (graph.cpp:13-56: sorted
+ * rows). edges = k (a, b) int64 label pairs (host). The graph stays on the
+ * device: tl_fetch_graph copies out offsets (n+1), adj (2m) and labels (n);
+ * tl_orient_normalized orients it with a device ordering (TL_ORDER_*). */
+TL_API tl_status tl_normalize(tl_ctx* ctx, uint64_t k, const int64_t* edges, uint32_t* n, uint64_t* m,
+                              uint64_t* loops_removed, uint64_t* duplicates_removed);
+TL_API tl_status tl_fetch_graph(tl_ctx* ctx, uint64_t* offsets, uint32_t* adj, int64_t* labels);
+TL_API tl_status tl_orient_normalized(tl_ctx* ctx, int method);
 /* Mismatched sizes (rank length != n) are reported as in oriented_view.cpp:8-9. */
 TL_API tl_status tl_check_sizes(uint32_t graph_n, uint32_t rank_n);
 

@@ -71,6 +71,10 @@ def ref() -> C.CDLL:
     L.ref_graph_from_csr.restype = _vp
     L.ref_graph_from_edges.argtypes = [_u32, _u64, _vp]
     L.ref_graph_from_edges.restype = _vp
+    L.ref_graph_normalize.argtypes = [_u64, _vp, C.POINTER(_u64), C.POINTER(_u64)]
+    L.ref_graph_normalize.restype = _vp
+    L.ref_graph_labels.argtypes = [_vp, _vp]
+    L.ref_graph_labels.restype = None
     L.ref_graph_gnm.argtypes = [_u32, _u64, _u64]
     L.ref_graph_gnm.restype = _vp
     L.ref_graph_random_small.argtypes = [_u64, _u32, _u64]
@@ -239,6 +243,24 @@ class RefGraph:
             e = np.zeros((1, 2), np.uint32)
             return cls(ref().ref_graph_from_edges(n, 0, e.ctypes.data))
         return cls(ref().ref_graph_from_edges(n, e.shape[0], e.ctypes.data))
+
+    @classmethod
+    def normalize(cls, raw_pairs):
+        """normalize (graph.cpp:115-151): returns (graph, loops_removed, duplicates_removed)."""
+        e = np.ascontiguousarray(np.asarray(raw_pairs, dtype=np.int64).reshape(-1, 2))
+        k = e.shape[0]
+        if k == 0:
+            e = np.zeros((1, 2), np.int64)
+        lo, du = C.c_uint64(0), C.c_uint64(0)
+        h = ref().ref_graph_normalize(k, e.ctypes.data, C.byref(lo), C.byref(du))
+        if not h:
+            raise ValueError(ref().ref_last_error().decode())
+        return cls(h), int(lo.value), int(du.value)
+
+    def labels(self) -> np.ndarray:
+        out = np.zeros(max(self.n, 1), np.int64)
+        ref().ref_graph_labels(self.h, out.ctypes.data)
+        return out[: self.n]
 
     def __del__(self):
         try:

@@ -159,6 +159,28 @@ void* ref_graph_from_edges(std::uint32_t n, std::uint64_t m, const std::uint32_t
     }
 }
 
+// The reference's normalize (graph.cpp:115-151) on raw labeled pairs; labels
+// of the result via ref_graph_labels.
+void* ref_graph_normalize(std::uint64_t k, const std::int64_t* ab, std::uint64_t* loops, std::uint64_t* dups) {
+    try {
+        std::vector<LabeledEdge> raw(k);
+        for (std::uint64_t i = 0; i < k; ++i) raw[i] = {ab[2 * i], ab[2 * i + 1]};
+        NormalizeStats st;
+        auto* g = new Graph(normalize(raw, &st));
+        *loops = st.loops_removed;
+        *dups = st.duplicates_removed;
+        return g;
+    } catch (const std::exception& e) {
+        g_error = e.what();
+        return nullptr;
+    }
+}
+
+void ref_graph_labels(void* gp, std::int64_t* out) {
+    const Graph& g = *static_cast<Graph*>(gp);
+    for (VertexId u = 0; u < g.vertex_count(); ++u) out[u] = g.label_of(u);
+}
+
 void* ref_graph_gnm(std::uint32_t n, std::uint64_t m, std::uint64_t seed) {
     try {
         return new Graph(gen_gnm(n, m, seed));

@@ -43,7 +43,7 @@ TRIGPU_SYMBOLS = (
     "tl_fetch_vertex_counts", "tl_fetch_oriented", "tl_cost_report",
     "tl_host_register", "tl_host_unregister", "tl_phase_times", "tl_phase_name",
     "tl_timer_start", "tl_timer_stop", "tl_order", "tl_order_device", "tl_orient_ordered",
-    "tl_fetch_ranks",
+    "tl_fetch_ranks", "tl_normalize", "tl_fetch_graph", "tl_orient_normalized",
 )
 
 
@@ -130,6 +130,13 @@ def trigpu() -> C.CDLL:
     lib.tl_orient_ordered.restype = C.c_int
     lib.tl_fetch_ranks.argtypes = [_vp, _vp]
     lib.tl_fetch_ranks.restype = C.c_int
+    lib.tl_normalize.argtypes = [_vp, _u64, _vp, C.POINTER(_u32), C.POINTER(_u64), C.POINTER(_u64),
+                                 C.POINTER(_u64)]
+    lib.tl_normalize.restype = C.c_int
+    lib.tl_fetch_graph.argtypes = [_vp, _vp, _vp, _vp]
+    lib.tl_fetch_graph.restype = C.c_int
+    lib.tl_orient_normalized.argtypes = [_vp, C.c_int]
+    lib.tl_orient_normalized.restype = C.c_int
     lib.tl_phase_name.argtypes = [C.c_int]
     lib.tl_phase_name.restype = C.c_char_p
     return lib

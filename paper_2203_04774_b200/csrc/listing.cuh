@@ -764,7 +764,7 @@ struct CtaCfg {
     static constexpr int kMinBlocks = MINB;
 };
 using CfgC1 = CtaCfg<256, 18, 14, 1024, 3>;
-using CfgC2 = CtaCfg<1024, 19, 15, 4096, 1>;
+using CfgC2 = CtaCfg<1024, 19, 15, 4096, 1>;  // (2 x 512-thread CTAs, 2^18 window: C5 5 % slower)
 template <class CFG>
 constexpr size_t cta_bitmap_bytes() { return win_bytes(CFG::kBitsA, CFG::kBitsB); }
 template <class CFG>

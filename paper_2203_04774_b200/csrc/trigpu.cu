@@ -26,6 +26,9 @@
 #include "listing.cuh"
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_select.cuh>
+
+#include "normalize.cuh"
 #include "orient.cuh"
 #include "segsort.cuh"
 #include "trigpu.h"
@@ -72,11 +75,14 @@ struct tl_ctx {
     uint32_t n = 0;
     uint64_t m = 0;
     bool oriented = false, in_built = false, hv_built = false;
+    bool normalized = false;  // goff / gadj / labels hold a tl_normalize result
+    uint32_t norm_n = 0;
+    uint64_t norm_m = 0;
     uint32_t max_out = 0;
     unsigned long long cost[4] = {0, 0, 0, 0};
     double h2d_ms = 0, orient_ms = 0;
 
-    DevBuf goff, gadj, rank, inv, hv, sort_tmp, radj, out_off, out_adj, in_off, in_adj, outdeg, indeg, lists, acc,
+    DevBuf goff, gadj, rank, inv, hv, sort_tmp, labels, radj, out_off, out_adj, in_off, in_adj, outdeg, indeg, lists, acc,
         vcount, tri, scan_part, bitmaps, small;
     bool have_vcounts = false, have_tri = false;
     int variant = 0;         // probe flavour (TRIGPU_VARIANT), for A/B measurement
@@ -501,7 +507,7 @@ TL_API void tl_destroy(tl_ctx* ctx) {
     DevBuf* bufs[] = {&ctx->goff,   &ctx->gadj,   &ctx->rank,  &ctx->inv,    &ctx->radj,      &ctx->out_off,
                       &ctx->out_adj, &ctx->in_off, &ctx->in_adj, &ctx->outdeg, &ctx->indeg,     &ctx->lists,
                       &ctx->acc,    &ctx->vcount, &ctx->tri,   &ctx->scan_part, &ctx->bitmaps, &ctx->small,
-                      &ctx->hv,     &ctx->sort_tmp};
+                      &ctx->hv,     &ctx->sort_tmp, &ctx->labels};
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     for (auto& ev : ctx->ev) cudaEventDestroy(ev);
@@ -621,6 +627,154 @@ TL_API tl_status tl_orient_ordered(tl_ctx* ctx, uint32_t n, uint64_t m, const ui
     st = orient_core(ctx, n, m, P<uint64_t>(ctx->goff), P<uint32_t>(ctx->gadj), P<uint32_t>(ctx->rank));
     if (st != TL_OK) return st;
     ctx->h2d_ms = ctx->phase_ms[PH_H2D] = ev_ms(ctx->ev[PH_COUNT + 2], ctx->ev[PH_H2D]);
+    return TL_OK;
+}
+
+// ---- raw edge list -> Graph CSR on the device (normalize, graph.cpp:115-151) --
+TL_API tl_status tl_normalize(tl_ctx* ctx, uint64_t k, const int64_t* edges, uint32_t* n_out, uint64_t* m_out,
+                              uint64_t* loops_removed, uint64_t* duplicates_removed) {
+    if (!ctx || (k && !edges) || !n_out || !m_out) return TL_ERR_INVALID_ARGUMENT;
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return ctx->cuda_fail("cudaSetDevice", cudaGetLastError());
+    ctx->normalized = false;
+    ctx->oriented = false;
+    if (k >= (1ull << 31)) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "normalize: more than 2^31 - 1 raw edges");
+    // scratch: raw (2k) | a, b (k each) | a2, b2 (k each) in radj-sized buffers
+    ENSURE(radj, std::max<size_t>(k * 16 * 3 + 64, 64));
+    ENSURE(small, 128);
+    auto* flags = static_cast<unsigned long long*>(ctx->small.p);
+    CK(cudaMemsetAsync(flags, 0, 64, ctx->s));
+    long long* raw = P<long long>(ctx->radj);
+    long long* a = raw + 2 * k;
+    long long* b = a + k;
+    long long* a2 = b + k;
+    long long* b2 = a2 + k;
+    if (k) CK(cudaMemcpyAsync(raw, edges, k * 16, cudaMemcpyHostToDevice, ctx->s));
+    const unsigned grid = grid_for(std::max<uint64_t>(k, 1), 256, ctx->sms * 16);
+    if (k) {
+        k_canon_edges<<<grid, 256, 0, ctx->s>>>(k, raw, a, b, flags);
+        LAUNCHED();
+    }
+    // sort by (a, b): stable LSD, first by b then by a; raw's space is free now
+    size_t tb = 0, tmp_bytes = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, b, b2, a, a2, (int)k, 0, 64, ctx->s));
+    tmp_bytes = std::max(tmp_bytes, tb);
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, a2, a, b2, b, (int)k, 0, 64, ctx->s));
+    tmp_bytes = std::max(tmp_bytes, tb);
+    ENSURE(sort_tmp, std::max<size_t>(tmp_bytes, k + 64) + 64);
+    if (k) {
+        CK(cub::DeviceRadixSort::SortPairs(ctx->sort_tmp.p, tmp_bytes, b, b2, a, a2, (int)k, 0, 64, ctx->s));
+        CK(cub::DeviceRadixSort::SortPairs(ctx->sort_tmp.p, tmp_bytes, a2, a, b2, b, (int)k, 0, 64, ctx->s));
+        ctx->launches += 16;
+    }
+    // first of each (a, b) run, not a loop -> compact into (a2, b2)
+    auto* keep = reinterpret_cast<unsigned char*>(raw);  // k bytes
+    auto* nsel = reinterpret_cast<int*>(flags + 2);
+    if (k) {
+        k_first_of_run<<<grid, 256, 0, ctx->s>>>(k, a, b, keep);
+        LAUNCHED();
+    }
+    tb = 0;
+    CK(cub::DeviceSelect::Flagged(nullptr, tb, a, keep, a2, nsel, (int)k, ctx->s));
+    if (tb > ctx->sort_tmp.cap) ENSURE(sort_tmp, tb + 64);
+    if (k) {
+        CK(cub::DeviceSelect::Flagged(ctx->sort_tmp.p, tb, a, keep, a2, nsel, (int)k, ctx->s));
+        CK(cub::DeviceSelect::Flagged(ctx->sort_tmp.p, tb, b, keep, b2, nsel, (int)k, ctx->s));
+        ctx->launches += 4;
+    } else {
+        CK(cudaMemsetAsync(nsel, 0, sizeof(int), ctx->s));
+    }
+    int m_i = 0;
+    unsigned long long loops = 0;
+    CK(cudaMemcpyAsync(&m_i, nsel, sizeof(int), cudaMemcpyDeviceToHost, ctx->s));
+    CK(cudaMemcpyAsync(&loops, flags, 8, cudaMemcpyDeviceToHost, ctx->s));
+    CK(cudaStreamSynchronize(ctx->s));
+    const uint64_t m = (uint64_t)m_i;
+    // labels: sorted distinct endpoints of the kept edges
+    long long* ends = a;        // 2m <= 2k words over a, b
+    long long* ends_sorted = raw;  // raw's 2k words
+    if (m) {
+        k_interleave_endpoints<<<grid_for(m, 256, ctx->sms * 16), 256, 0, ctx->s>>>(m, a2, b2, ends);
+        LAUNCHED();
+        tb = 0;
+        CK(cub::DeviceRadixSort::SortKeys(nullptr, tb, ends, ends_sorted, (int)(2 * m), 0, 64, ctx->s));
+        if (tb > ctx->sort_tmp.cap) ENSURE(sort_tmp, tb + 64);
+        CK(cub::DeviceRadixSort::SortKeys(ctx->sort_tmp.p, tb, ends, ends_sorted, (int)(2 * m), 0, 64, ctx->s));
+        ctx->launches += 8;
+    }
+    ENSURE(labels, std::max<uint64_t>(2 * m, 1) * 8);
+    long long* lab = P<long long>(ctx->labels);
+    int n_i = 0;
+    if (m) {
+        tb = 0;
+        CK(cub::DeviceSelect::Unique(nullptr, tb, ends_sorted, lab, nsel, (int)(2 * m), ctx->s));
+        if (tb > ctx->sort_tmp.cap) ENSURE(sort_tmp, tb + 64);
+        CK(cub::DeviceSelect::Unique(ctx->sort_tmp.p, tb, ends_sorted, lab, nsel, (int)(2 * m), ctx->s));
+        ctx->launches += 2;
+        CK(cudaMemcpyAsync(&n_i, nsel, sizeof(int), cudaMemcpyDeviceToHost, ctx->s));
+        CK(cudaStreamSynchronize(ctx->s));
+    }
+    const uint32_t n = (uint32_t)n_i;
+    // CSR: directed pair keys, one sort -> rows sorted; degrees -> offsets
+    ENSURE(goff, ((size_t)n + 1) * 8);
+    ENSURE(gadj, std::max<uint64_t>(2 * m, 1) * 4);
+    ENSURE(outdeg, (size_t)std::max<uint32_t>(n, 1) * 4);
+    auto* keys = reinterpret_cast<unsigned long long*>(raw);       // 2m words (raw region: 2k >= 2m)
+    auto* keys2 = reinterpret_cast<unsigned long long*>(a);        // 2m words over a, b
+    if (n) CK(cudaMemsetAsync(ctx->outdeg.p, 0, (size_t)n * 4, ctx->s));
+    if (m) {
+        k_dense_keys<<<grid_for(m, 256, ctx->sms * 16), 256, 0, ctx->s>>>(m, a2, b2, lab, n, keys,
+                                                                        P<uint32_t>(ctx->outdeg));
+        LAUNCHED();
+        const int hi_bits = 32 + std::max(1, 32 - __builtin_clz(std::max(n, 2u) - 1));
+        tb = 0;
+        CK(cub::DeviceRadixSort::SortKeys(nullptr, tb, keys, keys2, (int)(2 * m), 0, hi_bits, ctx->s));
+        if (tb > ctx->sort_tmp.cap) ENSURE(sort_tmp, tb + 64);
+        CK(cub::DeviceRadixSort::SortKeys(ctx->sort_tmp.p, tb, keys, keys2, (int)(2 * m), 0, hi_bits, ctx->s));
+        ctx->launches += 8;
+        k_low_words<<<grid_for(2 * m, 256, ctx->sms * 16), 256, 0, ctx->s>>>(2 * m, keys2, P<uint32_t>(ctx->gadj));
+        LAUNCHED();
+    }
+    tl_status st = scan_offsets(ctx, n, P<uint32_t>(ctx->outdeg), P<uint64_t>(ctx->goff));
+    if (st != TL_OK) return st;
+    CK(cudaStreamSynchronize(ctx->s));
+    ctx->normalized = true;
+    ctx->norm_n = n;
+    ctx->norm_m = m;
+    *n_out = n;
+    *m_out = m;
+    if (loops_removed) *loops_removed = loops;
+    if (duplicates_removed) *duplicates_removed = k - loops - m;
+    return TL_OK;
+}
+
+TL_API tl_status tl_fetch_graph(tl_ctx* ctx, uint64_t* offsets, uint32_t* adj, int64_t* labels) {
+    if (!ctx) return TL_ERR_INVALID_ARGUMENT;
+    if (!ctx->normalized) return ctx->fail(TL_ERR_STATE, "tl_fetch_graph: no normalized graph (call tl_normalize)");
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return ctx->cuda_fail("cudaSetDevice", cudaGetLastError());
+    const uint32_t n = ctx->norm_n;
+    const uint64_t m = ctx->norm_m;
+    if (offsets) CK(cudaMemcpyAsync(offsets, ctx->goff.p, ((size_t)n + 1) * 8, cudaMemcpyDeviceToHost, ctx->s));
+    if (adj && m) CK(cudaMemcpyAsync(adj, ctx->gadj.p, 2 * m * 4, cudaMemcpyDeviceToHost, ctx->s));
+    if (labels && n) CK(cudaMemcpyAsync(labels, ctx->labels.p, (size_t)n * 8, cudaMemcpyDeviceToHost, ctx->s));
+    CK(cudaStreamSynchronize(ctx->s));
+    return TL_OK;
+}
+
+// Orient the device-resident normalized graph with a device ordering: the
+// whole path raw edges -> listing without a host round trip.
+TL_API tl_status tl_orient_normalized(tl_ctx* ctx, int method) {
+    if (!ctx) return TL_ERR_INVALID_ARGUMENT;
+    if (!ctx->normalized) return ctx->fail(TL_ERR_STATE, "tl_orient_normalized: no normalized graph (call tl_normalize)");
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return ctx->cuda_fail("cudaSetDevice", cudaGetLastError());
+    const uint32_t n = ctx->norm_n;
+    ENSURE(rank, (size_t)n * 4 + 4);
+    tl_status st = order_core(ctx, n, P<uint64_t>(ctx->goff), method, P<uint32_t>(ctx->rank));
+    if (st != TL_OK) return st;
+    CK(cudaEventRecord(ctx->ev[PH_H2D], ctx->s));
+    st = orient_core(ctx, n, ctx->norm_m, P<uint64_t>(ctx->goff), P<uint32_t>(ctx->gadj), P<uint32_t>(ctx->rank));
+    if (st != TL_OK) return st;
+    ctx->h2d_ms = ctx->phase_ms[PH_H2D] = 0;
+    ctx->normalized = true;  // goff / gadj untouched by orientation
     return TL_OK;
 }
 

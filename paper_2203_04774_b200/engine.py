@@ -120,6 +120,28 @@ class Context:
                                                            offsets.ctypes.data, adj.ctypes.data,
                                                            self._ORDERS[method]))
 
+    def normalize(self, raw_pairs) -> tuple[int, int, int, int]:
+        """Raw labeled edges -> Graph CSR on the device (normalize, graph.cpp:115-151).
+        Returns (n, m, loops_removed, duplicates_removed); tl_fetch_graph reads it."""
+        e = np.ascontiguousarray(np.asarray(raw_pairs, dtype=np.int64).reshape(-1, 2))
+        n, m, lo, du = C.c_uint32(0), C.c_uint64(0), C.c_uint64(0), C.c_uint64(0)
+        _check(self._p, _native.trigpu().tl_normalize(self._p, e.shape[0], e.ctypes.data if e.shape[0] else None,
+                                                      C.byref(n), C.byref(m), C.byref(lo), C.byref(du)))
+        self._norm = (int(n.value), int(m.value))
+        return int(n.value), int(m.value), int(lo.value), int(du.value)
+
+    def fetch_graph(self):
+        """(offsets uint64[n+1], adjacency uint32[2m], labels int64[n]) of the last normalize."""
+        n, m = self._norm
+        off = np.zeros(n + 1, np.uint64)
+        adj = np.zeros(max(2 * m, 1), np.uint32)
+        lab = np.zeros(max(n, 1), np.int64)
+        _check(self._p, _native.trigpu().tl_fetch_graph(self._p, off.ctypes.data, adj.ctypes.data, lab.ctypes.data))
+        return off, adj[: 2 * m], lab[:n]
+
+    def orient_normalized(self, method: str) -> None:
+        _check(self._p, _native.trigpu().tl_orient_normalized(self._p, self._ORDERS[method]))
+
     def fetch_ranks(self, n: int) -> np.ndarray:
         rank = np.empty(max(n, 1), dtype=np.uint32)
         _check(self._p, _native.trigpu().tl_fetch_ranks(self._p, rank.ctypes.data))
