@@ -132,6 +132,15 @@ TL_API tl_status tl_list(tl_ctx* ctx, int algo, unsigned out_flags, tl_stats* ou
  * rank-ascending (u, v, w), triples in unspecified order. cap in triangles.
  * TL_ERR_CAPACITY (with *k set) when cap is too small. */
 TL_API tl_status tl_fetch_triangles(tl_ctx* ctx, uint32_t* uvw, uint64_t cap, uint64_t* k);
+/* Chunked reads of the same list, so a caller can stream
+ * a list larger than its buffers to disk: triangles [first, first + k) with
+ * k = min(cap, total - first), as dense ids, or mapped to the Graph's int64
+ * labels (the CLI's --out writes labels, trilist_cli.cpp:212-220). labels =
+ * the label table (int64[n], host), or NULL for the labels of the last
+ * tl_normalize when the oriented graph is that graph. */
+TL_API tl_status tl_fetch_triangles_range(tl_ctx* ctx, uint64_t first, uint64_t cap, uint32_t* uvw, uint64_t* k);
+TL_API tl_status tl_fetch_triangle_labels(tl_ctx* ctx, uint64_t first, uint64_t cap, const int64_t* labels,
+                                          int64_t* out, uint64_t* k);
 /* Per-vertex triangle counts (dense ids) of the last TL_OUT_VERTEX_COUNTS run. */
 TL_API tl_status tl_fetch_vertex_counts(tl_ctx* ctx, uint64_t* counts);
 /* The oriented view in the reference layout (oriented_view.hpp:41-45):

@@ -44,6 +44,7 @@ TRIGPU_SYMBOLS = (
     "tl_host_register", "tl_host_unregister", "tl_phase_times", "tl_phase_name",
     "tl_timer_start", "tl_timer_stop", "tl_order", "tl_order_device", "tl_orient_ordered",
     "tl_fetch_ranks", "tl_normalize", "tl_fetch_graph", "tl_orient_normalized",
+    "tl_fetch_triangles_range", "tl_fetch_triangle_labels",
 )
 
 
@@ -135,6 +136,10 @@ def trigpu() -> C.CDLL:
     lib.tl_normalize.restype = C.c_int
     lib.tl_fetch_graph.argtypes = [_vp, _vp, _vp, _vp]
     lib.tl_fetch_graph.restype = C.c_int
+    lib.tl_fetch_triangles_range.argtypes = [_vp, _u64, _u64, _vp, C.POINTER(_u64)]
+    lib.tl_fetch_triangles_range.restype = C.c_int
+    lib.tl_fetch_triangle_labels.argtypes = [_vp, _u64, _u64, _vp, _vp, C.POINTER(_u64)]
+    lib.tl_fetch_triangle_labels.restype = C.c_int
     lib.tl_orient_normalized.argtypes = [_vp, C.c_int]
     lib.tl_orient_normalized.restype = C.c_int
     lib.tl_phase_name.argtypes = [C.c_int]

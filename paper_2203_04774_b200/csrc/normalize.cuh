@@ -90,4 +90,11 @@ __global__ void k_low_words(uint64_t k, const unsigned long long* __restrict__ k
         adj[i] = static_cast<uint32_t>(keys[i]);
 }
 
+// out[i] = labels[ids[i]] (list output mapped to the Graph's labels)
+__global__ void k_map_labels(uint64_t cnt, const uint32_t* __restrict__ ids, const long long* __restrict__ labels,
+                             long long* __restrict__ out) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cnt; i += stride) out[i] = labels[ids[i]];
+}
+
 }  // namespace trigpu

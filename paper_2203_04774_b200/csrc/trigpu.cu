@@ -926,6 +926,45 @@ TL_API tl_status tl_fetch_triangles(tl_ctx* ctx, uint32_t* uvw, uint64_t cap, ui
     return TL_OK;
 }
 
+TL_API tl_status tl_fetch_triangles_range(tl_ctx* ctx, uint64_t first, uint64_t cap, uint32_t* uvw, uint64_t* k) {
+    if (!ctx || !k) return TL_ERR_INVALID_ARGUMENT;
+    if (!ctx->have_tri) return ctx->fail(TL_ERR_STATE, "tl_fetch_triangles_range: last tl_list did not use TL_OUT_LIST");
+    *k = first < ctx->tri_count ? std::min<uint64_t>(cap, ctx->tri_count - first) : 0;
+    if (*k) {
+        if (!uvw) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "tl_fetch_triangles_range: null buffer");
+        if (cudaSetDevice(ctx->device) != cudaSuccess) return ctx->cuda_fail("cudaSetDevice", cudaGetLastError());
+        CK(cudaMemcpyAsync(uvw, P<uint32_t>(ctx->tri) + 3 * first, *k * 12, cudaMemcpyDeviceToHost, ctx->s));
+        CK(cudaStreamSynchronize(ctx->s));
+    }
+    return TL_OK;
+}
+
+TL_API tl_status tl_fetch_triangle_labels(tl_ctx* ctx, uint64_t first, uint64_t cap, const int64_t* labels,
+                                          int64_t* out, uint64_t* k) {
+    if (!ctx || !k) return TL_ERR_INVALID_ARGUMENT;
+    if (!ctx->have_tri) return ctx->fail(TL_ERR_STATE, "tl_fetch_triangle_labels: last tl_list did not use TL_OUT_LIST");
+    if (!labels && !(ctx->normalized && ctx->norm_n == ctx->n))
+        return ctx->fail(TL_ERR_STATE, "tl_fetch_triangle_labels: no label table (pass one, or orient a tl_normalize graph)");
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return ctx->cuda_fail("cudaSetDevice", cudaGetLastError());
+    *k = first < ctx->tri_count ? std::min<uint64_t>(cap, ctx->tri_count - first) : 0;
+    if (!*k) return TL_OK;
+    if (!out) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "tl_fetch_triangle_labels: null buffer");
+    const long long* lab = P<long long>(ctx->labels);
+    if (labels) {  // caller's table: stage it after the normalize labels' slot
+        ENSURE(sort_tmp, (size_t)ctx->n * 8 + 64);
+        CK(cudaMemcpyAsync(ctx->sort_tmp.p, labels, (size_t)ctx->n * 8, cudaMemcpyHostToDevice, ctx->s));
+        lab = P<long long>(ctx->sort_tmp);
+        ctx->normalized = false;  // sort_tmp is normalize's scratch; the graph itself stays valid
+    }
+    ENSURE(scan_part, *k * 24);
+    k_map_labels<<<grid_for(*k * 3, 256, ctx->sms * 16), 256, 0, ctx->s>>>(*k * 3, P<uint32_t>(ctx->tri) + 3 * first, lab,
+                                                                          P<long long>(ctx->scan_part));
+    LAUNCHED();
+    CK(cudaMemcpyAsync(out, ctx->scan_part.p, *k * 24, cudaMemcpyDeviceToHost, ctx->s));
+    CK(cudaStreamSynchronize(ctx->s));
+    return TL_OK;
+}
+
 TL_API tl_status tl_fetch_vertex_counts(tl_ctx* ctx, uint64_t* counts) {
     if (!ctx) return TL_ERR_INVALID_ARGUMENT;
     if (!ctx->have_vcounts) return ctx->fail(TL_ERR_STATE, "tl_fetch_vertex_counts: last tl_list did not use TL_OUT_VERTEX_COUNTS");

@@ -139,6 +139,26 @@ class Context:
         _check(self._p, _native.trigpu().tl_fetch_graph(self._p, off.ctypes.data, adj.ctypes.data, lab.ctypes.data))
         return off, adj[: 2 * m], lab[:n]
 
+    def iter_triangles(self, chunk: int = 1 << 24, labels: np.ndarray | None = None, use_labels: bool = False):
+        """Stream the last TL_OUT_LIST result in chunks: uint32 (k, 3) dense ids,
+        or int64 labels (labels=table, or use_labels=True for the tl_normalize labels)."""
+        first = 0
+        k = C.c_uint64(0)
+        lab = None if labels is None else np.ascontiguousarray(labels, dtype=np.int64)
+        while True:
+            if lab is None and not use_labels:
+                buf = np.empty((chunk, 3), np.uint32)
+                _check(self._p, _native.trigpu().tl_fetch_triangles_range(self._p, first, chunk, buf.ctypes.data,
+                                                                          C.byref(k)))
+            else:
+                buf = np.empty((chunk, 3), np.int64)
+                _check(self._p, _native.trigpu().tl_fetch_triangle_labels(
+                    self._p, first, chunk, lab.ctypes.data if lab is not None else None, buf.ctypes.data, C.byref(k)))
+            if k.value == 0:
+                return
+            yield buf[: k.value]
+            first += k.value
+
     def orient_normalized(self, method: str) -> None:
         _check(self._p, _native.trigpu().tl_orient_normalized(self._p, self._ORDERS[method]))
 

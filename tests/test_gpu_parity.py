@@ -357,3 +357,34 @@ def test_device_normalize_matches_reference():
             assert (st.triangle_count, st.checksum) == (exp.triangle_count, exp.checksum)
     finally:
         c.close()
+
+
+def test_chunked_triangle_stream_with_labels():
+    """tl_fetch_triangles_range / tl_fetch_triangle_labels stream the list in
+    chunks; concatenated they equal tl_fetch_triangles, and mapped through
+    the Graph's labels they equal the reference's labelled triangle set."""
+    rng = np.random.default_rng(5)
+    g = tg.gen_rmat(12, 16, 9)
+    e = np.stack([np.repeat(np.arange(g.n), np.diff(g.offsets.astype(np.int64))), g.adjacency], 1)
+    labels_of = rng.permutation(np.arange(g.n, dtype=np.int64) * 7919 - 10**6)
+    raw = labels_of[e]
+    c = tg.Context(0)
+    try:
+        n, m, _, _ = c.normalize(raw)
+        off, adj, labels = c.fetch_graph()
+        c.orient_normalized("degree")
+        st = c.list(TL_ALGO_APM, TL_OUT_LIST)
+        whole = c.fetch_triangles()
+        parts = np.concatenate(list(c.iter_triangles(chunk=1000)))
+        assert np.array_equal(parts, whole) and parts.shape[0] == st.triangle_count
+        lab_parts = np.concatenate(list(c.iter_triangles(chunk=777, use_labels=True)))
+        assert np.array_equal(lab_parts, labels[whole])
+        lab2 = np.concatenate(list(c.iter_triangles(chunk=5000, labels=labels)))
+        assert np.array_equal(lab2, lab_parts)
+        rg, _, _ = oracle.RefGraph.normalize(raw)
+        exp = oracle.RefView(rg, rg.order("degree")).list(TL_ALGO_APM, collect=True)
+        exp_lab = np.sort(rg.labels()[exp.triangles], axis=1)
+        got = np.sort(lab_parts, axis=1)
+        assert np.array_equal(got[np.lexsort(got.T[::-1])], exp_lab[np.lexsort(exp_lab.T[::-1])])
+    finally:
+        c.close()
