@@ -369,7 +369,7 @@ __device__ __forceinline__ void stream_quads(const ListParams& P, uint32_t seed,
             pr[i] = lane < ch[i].nq;
             a[i] = quads + (ch[i].qb + lane);
         }
-        ldgq(a, pr, y);
+        ldgq<!kSparse>(a, pr, y);
         uint32_t hb[QU];
         bool any = false;
 #pragma unroll
