@@ -11,8 +11,8 @@
 //
 // The reference's uint8 table[n] (listing.hpp:113) becomes a per-seed
 // windowed bitmap in shared memory sized to the class of |S| (degree binning):
-//   class R  2 <= |S| <= 32     warp per seed, 2^13-bit window per warp
-//   class H  32 < |S| <= 256    warp per seed, 2^15-bit window per warp
+//   class R  2 <= |S| <= 32     warp per seed, 2^15-bit window per warp
+//   class H  32 < |S| <= 256    warp per seed, 2^16-bit window per warp
 //   class C1 256 < |S| <= 1024  CTA (8 warps) per seed, 2^18-bit window
 //   class C2 1024 < |S| <= 4096 CTA (32 warps) per seed, 2^19-bit window
 //   class G  |S| > 4096         CTA per seed, n-bit bitmap in global memory
@@ -668,7 +668,10 @@ __device__ __forceinline__ void attach_scratch(Sink<ALGO, F>& sink, unsigned cha
 
 // ---- class R: |S| <= 32, warp per seed --------------------------------------
 constexpr int kRWarps = 8;
-constexpr uint32_t kRBitsA = 13, kRBitsB = 11;  // 1 KB window + 256 B region B per warp
+#ifndef TRIGPU_R_BITS_A
+#define TRIGPU_R_BITS_A 15
+#endif
+constexpr uint32_t kRBitsA = TRIGPU_R_BITS_A, kRBitsB = 11;  // 4 KB window + 256 B region B per warp
 constexpr size_t kRBmBytes = win_bytes(kRBitsA, kRBitsB);
 
 template <int ALGO, unsigned F>
