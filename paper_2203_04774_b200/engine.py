@@ -273,7 +273,7 @@ class CountingSink:
 
 class ChecksumSink(CountingSink):
     """Order-independent checksum: wrapping sum over triangles of
-    mix64(mix64(mix64(a) ^ b) ^ c), (a, b, c) the dense ids sorted."""
+    h(a) * h(b) * h(c) mod 2^64, h(v) = mix64(v) | 1, (a, b, c) the dense ids."""
 
     flags = TL_OUT_CHECKSUM
 
