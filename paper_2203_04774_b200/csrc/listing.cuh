@@ -766,11 +766,7 @@ struct CtaCfg {
     static constexpr uint32_t kMaxD = MAXD;
     static constexpr int kMinBlocks = MINB;
 };
-#ifdef TRIGPU_C1_EXP
-using CfgC1 = CtaCfg<256, 17, 14, 1024, 4>;  // A/B: 16 KB window, 4 CTAs/SM at 64 registers
-#else
-using CfgC1 = CtaCfg<256, 18, 14, 1024, 3>;
-#endif
+using CfgC1 = CtaCfg<256, 18, 14, 1024, 3>;  // (2^17 window at 4 CTAs/SM: C4 -1 %, C5 +4 %)
 using CfgC2 = CtaCfg<1024, 19, 15, 4096, 1>;  // (2 x 512-thread CTAs, 2^18 window: C5 5 % slower)
 template <class CFG>
 constexpr size_t cta_bitmap_bytes() { return win_bytes(CFG::kBitsA, CFG::kBitsB); }
