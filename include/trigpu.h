@@ -167,6 +167,17 @@ TL_API tl_status tl_timer_stop(tl_ctx* ctx, double* ms);
 TL_API int tl_phase_times(const tl_ctx* ctx, double* ms, int cap);
 TL_API const char* tl_phase_name(int i);
 
+/* Test-only knobs (not part of the reference interface; the product never
+ * reads the environment):
+ *   TL_DEBUG_BM_SHRINK  shrink every seed's shared-memory window and filter by
+ *                       2^value so graphs small enough for the oracle take the
+ *                       below-window (filter + exact verification) path;
+ *   TL_DEBUG_VARIANT    probe variant of a -DTRIGPU_EXPERIMENTS build (2 = null
+ *                       probe, timing only); ignored otherwise.
+ * Settings persist for the context. */
+enum { TL_DEBUG_BM_SHRINK = 1, TL_DEBUG_VARIANT = 2 };
+TL_API tl_status tl_debug_set(tl_ctx* ctx, int key, int value);
+
 #ifdef __cplusplus
 }
 #endif

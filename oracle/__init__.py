@@ -56,6 +56,9 @@ def lib() -> C.CDLL:
     L.or_brute.restype = _u64
     L.or_canonicalize.argtypes = [_vp, _u64]
     L.or_canonicalize.restype = None
+    L.or_list_ranges.argtypes = [C.c_int, _u32, _vp, _vp, _vp, _vp, _vp, _vp, _u64, C.c_int,
+                                 C.POINTER(OrStats)]
+    L.or_list_ranges.restype = C.c_int
     return L
 
 
@@ -98,6 +101,17 @@ def ref() -> C.CDLL:
     L.ref_list.argtypes = [_vp, C.c_int, C.c_int, _u32, _u32, _vp, _vp, _u64, C.POINTER(_u64),
                            C.POINTER(RefStats)]
     L.ref_list.restype = C.c_int
+    L.ref_list_ranges.argtypes = [_vp, C.c_int, C.c_int, _vp, _u64, C.POINTER(RefStats)]
+    L.ref_list_ranges.restype = C.c_int
+    # synthetic-graph generators (trihost.cpp compiled into this library)
+    L.th_last_error.restype = C.c_char_p
+    L.th_gen_gnm.argtypes = [_u32, _u64, _u64, _vp]
+    L.th_gen_rmat.argtypes = [_u32, _u32, _u64, _vp]
+    L.th_gen_chung_lu.argtypes = [_u32, _u64, C.c_double, C.c_double, C.c_double, _u64, _vp]
+    L.th_gen_ws.argtypes = [_u32, _u32, C.c_double, _u64, _vp]
+    L.th_csr_free.argtypes = [_vp]
+    for f in (L.th_gen_gnm, L.th_gen_rmat, L.th_gen_chung_lu, L.th_gen_ws):
+        f.restype = C.c_int
     L.ref_brute.argtypes = [_vp, _u32, _vp, _u64]
     L.ref_brute.restype = C.c_int64
     return L
@@ -182,6 +196,20 @@ def list_triangles(view: OrientedCSR, algo: int, threads: int = 1, vcounts: bool
                       int(st.checksum), float(st.wall_ms),
                       vc[:n] if vc is not None else None,
                       tri[:k] if tri is not None else None)
+
+
+def list_ranges(view: OrientedCSR, algo: int, ranges, threads: int = 1) -> ListResult:
+    """or_list_ranges: count + checksum over a sample of rank ranges, one pass."""
+    n = view.succ_off.shape[0] - 1
+    r = np.ascontiguousarray(np.asarray(ranges, dtype=np.uint32).reshape(-1, 2))
+    st = OrStats()
+    succ = view.succ if view.succ.shape[0] else np.zeros(1, np.uint32)
+    pred = view.pred if view.pred.shape[0] else np.zeros(1, np.uint32)
+    lib().or_list_ranges(algo, n, view.succ_off.ctypes.data, succ.ctypes.data, view.pred_off.ctypes.data,
+                         pred.ctypes.data, view.inverse.ctypes.data, r.ctypes.data, r.shape[0], threads,
+                         C.byref(st))
+    return ListResult(int(st.triangle_count), int(st.inner_ops), int(st.mark_ops), int(st.checksum),
+                      float(st.wall_ms))
 
 
 def cost(view: OrientedCSR) -> tuple[int, int, int, int]:
@@ -321,6 +349,16 @@ class RefView:
         except Exception:
             pass
 
+    def list_ranges(self, algo: int, ranges, threads: int = 1) -> ListResult:
+        """The reference's run_*_range loops over a sample of rank ranges in one
+        run_parallel-style pulling pass (ref_list_ranges)."""
+        r = np.ascontiguousarray(np.asarray(ranges, dtype=np.uint32).reshape(-1, 2))
+        st = RefStats()
+        if ref().ref_list_ranges(self.h, algo, threads, r.ctypes.data, r.shape[0], C.byref(st)) != 0:
+            raise ValueError(ref().ref_last_error().decode())
+        return ListResult(int(st.triangle_count), int(st.inner_ops), int(st.mark_ops), int(st.checksum),
+                          float(st.wall_ms))
+
     def csr(self):
         so = np.zeros(self.n + 1, np.uint64)
         po = np.zeros(self.n + 1, np.uint64)
@@ -358,3 +396,48 @@ class RefView:
                           int(st.checksum), float(st.wall_ms),
                           vc[: self.n] if vc is not None else None,
                           tri[: min(k.value, cap)] if tri is not None else None)
+
+
+# -- synthetic inputs for the reference arm ------------------------------------------
+
+class _ThCsr(C.Structure):
+    _fields_ = [("n", C.c_uint32), ("m", C.c_uint64), ("offsets", C.POINTER(C.c_uint64)),
+                ("adj", C.POINTER(C.c_uint32))]
+
+
+class GenGraph:
+    """A BASELINE config graph (offsets uint64[n+1], adjacency uint32[2m]) from
+    the same counter-based generators the engine's host side uses, built into
+    _ref/libtrilist_ref.so so the reference arm loads nothing outside oracle/."""
+
+    def __init__(self, kind: str, **kw):
+        csr = _ThCsr()
+        L = ref()
+        if kind == "gnm":
+            rc = L.th_gen_gnm(kw["n"], kw["m"], kw["seed"], C.byref(csr))
+        elif kind == "rmat":
+            rc = L.th_gen_rmat(kw["scale"], kw["ef"], kw["seed"], C.byref(csr))
+        elif kind == "chung_lu":
+            rc = L.th_gen_chung_lu(kw["n"], kw["draws"], 2.1, 2.0, 50000.0, kw["seed"], C.byref(csr))
+        elif kind == "ws":
+            rc = L.th_gen_ws(kw["n"], kw["k"], kw["p"], kw["seed"], C.byref(csr))
+        else:
+            raise ValueError(kind)
+        if rc != 0:
+            raise RuntimeError(L.th_last_error().decode())
+        self._csr = csr
+        self.n, self.m = int(csr.n), int(csr.m)
+        self.offsets = np.ctypeslib.as_array(csr.offsets, shape=(self.n + 1,))
+        self.adjacency = np.ctypeslib.as_array(csr.adj, shape=(max(2 * self.m, 1),))[: 2 * self.m]
+
+    def free(self):
+        if self._csr is not None:
+            self.offsets = self.adjacency = None
+            ref().th_csr_free(C.byref(self._csr))
+            self._csr = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass

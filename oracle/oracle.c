@@ -86,6 +86,9 @@ typedef struct {
     uint64_t tri_cap;
     volatile uint64_t tri_cursor;
     volatile uint32_t next_block; /* listing.hpp:126 */
+    const uint32_t* ranges;       /* optional sample: [ranges[2i], ranges[2i+1]) */
+    uint64_t nranges;
+    volatile uint64_t next_sub;   /* 1024-rank sub-block cursor over the sample */
     pthread_mutex_t lock;
     or_stats total;
 } list_job;
@@ -162,7 +165,26 @@ static void* lane_main(void* arg) {
     list_job* J = (list_job*)arg;
     uint8_t* table = (uint8_t*)calloc(J->n ? J->n : 1, 1);
     lane_acc acc = {0, 0, 0, 0};
-    for (;;) {
+    while (J->ranges) {  /* sample mode: pull 1024-rank sub-blocks of the ranges */
+        const uint64_t k = __atomic_fetch_add(&J->next_sub, 1u, __ATOMIC_RELAXED);
+        uint64_t acc_blocks = 0, i = 0;
+        uint32_t b = 0, e = 0;
+        for (; i < J->nranges; ++i) {
+            const uint32_t rb = J->ranges[2 * i];
+            const uint32_t re = J->ranges[2 * i + 1] > J->n ? J->n : J->ranges[2 * i + 1];
+            const uint64_t nb = re > rb ? (re - rb + 1023u) / 1024u : 0;
+            if (k < acc_blocks + nb) {
+                b = rb + (uint32_t)(k - acc_blocks) * 1024u;
+                e = re - b > 1024u ? b + 1024u : re;
+                break;
+            }
+            acc_blocks += nb;
+        }
+        if (i == J->nranges) break;
+        if (J->algo == OR_ALGO_APP) run_app_range(J, b, e, table, &acc);
+        else run_apm_range(J, b, e, table, &acc);
+    }
+    for (; !J->ranges;) {
         const uint32_t span = J->rank_end - J->rank_begin;
         const uint32_t off = __atomic_fetch_add(&J->next_block, 1024u, __ATOMIC_RELAXED);
         if (off >= span) break;
@@ -222,6 +244,35 @@ uint64_t or_list(int algo, uint32_t n, const uint64_t* succ_off, const uint32_t*
     pthread_mutex_destroy(&J.lock);
     if (out) *out = J.total;
     return J.tri_cursor < J.tri_cap ? J.tri_cursor : J.tri_cap;
+}
+
+/* Count + checksum over a sample of rank ranges (bench.py's cpu_baseline:
+ * one pulling pass over all sampled blocks, tables allocated once per lane). */
+int or_list_ranges(int algo, uint32_t n, const uint64_t* succ_off, const uint32_t* succ,
+                   const uint64_t* pred_off, const uint32_t* pred, const uint32_t* inverse,
+                   const uint32_t* ranges, uint64_t nranges, int threads, or_stats* out) {
+    list_job J;
+    memset(&J, 0, sizeof(J));
+    J.algo = algo;
+    J.n = n;
+    J.succ_off = succ_off;
+    J.succ = succ;
+    J.pred_off = pred_off;
+    J.pred = pred;
+    J.inverse = inverse;
+    J.ranges = ranges;
+    J.nranges = nranges;
+    pthread_mutex_init(&J.lock, NULL);
+    if (threads < 1) threads = 1;
+    const double t0 = now_ms();
+    pthread_t* pool = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)threads);
+    for (int t = 0; t < threads; ++t) pthread_create(&pool[t], NULL, lane_main, &J);
+    for (int t = 0; t < threads; ++t) pthread_join(pool[t], NULL);
+    free(pool);
+    J.total.wall_ms = now_ms() - t0;
+    pthread_mutex_destroy(&J.lock);
+    if (out) *out = J.total;
+    return 0;
 }
 
 void or_cost(uint32_t n, const uint64_t* succ_off, const uint64_t* pred_off, uint64_t out[4]) {

@@ -61,6 +61,11 @@ uint64_t or_list(int algo, uint32_t n, const uint64_t* succ_off, const uint32_t*
                  uint64_t* vcounts, uint32_t* tri, uint64_t tri_cap, or_stats* out);
 
 /* cost_report(view) (reference cost.cpp:27-38): out = {c_pp, c_pm, c_mm, sum_deg_sq}. */
+/* or_list over a sample of rank ranges [ranges[2i], ranges[2i+1]) in one
+ * pulling pass (count + checksum only). */
+int or_list_ranges(int algo, uint32_t n, const uint64_t* succ_off, const uint32_t* succ,
+                   const uint64_t* pred_off, const uint32_t* pred, const uint32_t* inverse,
+                   const uint32_t* ranges, uint64_t nranges, int threads, or_stats* out);
 void or_cost(uint32_t n, const uint64_t* succ_off, const uint64_t* pred_off, uint64_t out[4]);
 
 /* brute_triangles(g) (reference oracle.cpp:12-30) without the guard: sorted

@@ -123,6 +123,39 @@ ListingStats ranged_parallel(const OrientedView& view, Runner runner, HarnessSin
     return total;
 }
 
+// The same pulling over an explicit list of rank sub-blocks (each <= 1024
+// ranks): a bounded sample of the workload listed in ONE run_parallel-style
+// call, so the per-call setup (a zeroed table(n) per lane, listing.hpp:134)
+// is paid once per sample, as it is once per full listing.
+template <typename Runner>
+ListingStats blocks_parallel(const OrientedView& view, Runner runner, HarnessSink& sink, unsigned threads,
+                             const std::vector<std::pair<VertexId, VertexId>>& blocks) {
+    const VertexId n = view.vertex_count();
+    std::atomic<std::size_t> next{0};
+    std::mutex mu;
+    ListingStats total;
+    const auto t0 = std::chrono::steady_clock::now();
+    auto worker = [&] {
+        ListingStats local;
+        HarnessSink local_sink;
+        std::vector<std::uint8_t> table(n, 0);
+        for (;;) {
+            const std::size_t i = next.fetch_add(1);
+            if (i >= blocks.size()) break;
+            runner(view, blocks[i].first, blocks[i].second, table, local_sink, local);
+        }
+        std::lock_guard<std::mutex> lock(mu);
+        total.merge(local);
+        sink.merge(std::move(local_sink));
+    };
+    std::vector<std::thread> pool;
+    for (unsigned t = 0; t < std::max(1u, threads); ++t) pool.emplace_back(worker);
+    for (auto& t : pool) t.join();
+    total.wall_ms = std::chrono::duration<double, std::milli>(
+                        std::chrono::steady_clock::now() - t0).count();
+    return total;
+}
+
 }  // namespace
 
 extern "C" {
@@ -357,6 +390,44 @@ int ref_list(void* vp, int algo, int threads, std::uint32_t rank_begin, std::uin
             }
             *k = sink.triangles.size();
         }
+        return 0;
+    } catch (const std::exception& e) {
+        g_error = e.what();
+        return -1;
+    }
+}
+
+// Count + checksum over a sample of rank ranges ([ranges[2i], ranges[2i+1])),
+// cut into 1024-rank blocks and pulled by `threads` lanes in one call.
+int ref_list_ranges(void* vp, int algo, int threads, const std::uint32_t* ranges, std::uint64_t nranges,
+                    ref_stats* out) {
+    try {
+        const OrientedView& view = *static_cast<OrientedView*>(vp);
+        const VertexId n = view.vertex_count();
+        g_cfg.vcounts = false;
+        g_cfg.collect = false;
+        g_cfg.n = n;
+        std::vector<std::pair<VertexId, VertexId>> blocks;
+        for (std::uint64_t i = 0; i < nranges; ++i) {
+            const VertexId rb = ranges[2 * i], re = std::min<VertexId>(ranges[2 * i + 1], n);
+            for (std::uint64_t b = rb; b < re; b += 1024)
+                blocks.emplace_back(static_cast<VertexId>(b), static_cast<VertexId>(std::min<std::uint64_t>(re, b + 1024)));
+        }
+        HarnessSink sink;
+        ListingStats st;
+        if (algo == 0)
+            st = blocks_parallel(
+                view, [](auto&&... a) { detail::run_app_range(std::forward<decltype(a)>(a)...); }, sink,
+                static_cast<unsigned>(threads), blocks);
+        else
+            st = blocks_parallel(
+                view, [](auto&&... a) { detail::run_apm_range(std::forward<decltype(a)>(a)...); }, sink,
+                static_cast<unsigned>(threads), blocks);
+        out->triangle_count = st.triangle_count;
+        out->inner_ops = st.inner_ops;
+        out->mark_ops = st.mark_ops;
+        out->checksum = sink.checksum;
+        out->wall_ms = st.wall_ms;
         return 0;
     } catch (const std::exception& e) {
         g_error = e.what();

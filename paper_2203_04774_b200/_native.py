@@ -35,6 +35,8 @@ TL_OUT_COUNT = 0
 TL_OUT_CHECKSUM = 1
 TL_OUT_VERTEX_COUNTS = 2
 TL_OUT_LIST = 4
+TL_DEBUG_BM_SHRINK = 1
+TL_DEBUG_VARIANT = 2
 
 # every exported symbol of include/trigpu.h (tests check the .so exports all)
 TRIGPU_SYMBOLS = (
@@ -44,7 +46,7 @@ TRIGPU_SYMBOLS = (
     "tl_host_register", "tl_host_unregister", "tl_phase_times", "tl_phase_name",
     "tl_timer_start", "tl_timer_stop", "tl_order", "tl_order_device", "tl_orient_ordered",
     "tl_fetch_ranks", "tl_normalize", "tl_fetch_graph", "tl_orient_normalized",
-    "tl_fetch_triangles_range", "tl_fetch_triangle_labels",
+    "tl_fetch_triangles_range", "tl_fetch_triangle_labels", "tl_debug_set",
 )
 
 
@@ -144,6 +146,8 @@ def trigpu() -> C.CDLL:
     lib.tl_orient_normalized.restype = C.c_int
     lib.tl_phase_name.argtypes = [C.c_int]
     lib.tl_phase_name.restype = C.c_char_p
+    lib.tl_debug_set.argtypes = [_vp, C.c_int, C.c_int]
+    lib.tl_debug_set.restype = C.c_int
     return lib
 
 

@@ -80,51 +80,12 @@ __device__ __forceinline__ uint32_t lds32(unsigned a) {
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
     return v;
 }
-__device__ __forceinline__ void sts32(unsigned a, uint32_t v) {
-    asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
-}
 __device__ __forceinline__ void sts128(unsigned a, uint4 v) {
     asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                  : "memory");
 }
 __device__ __forceinline__ void sts64(unsigned a, uint2 v) {
     asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(v.x), "r"(v.y) : "memory");
-}
-
-// Predicated shared loads: the value stays `dflt` when !p (no branch).
-__device__ __forceinline__ uint32_t lds32_if(unsigned a, bool p, uint32_t dflt = 0u) {
-    uint32_t v = dflt;
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.shared.u32 %0, [%1];\n\t}"
-                 : "+r"(v)
-                 : "r"(a), "r"((unsigned)p));
-    return v;
-}
-
-// Eight independent read-only global loads issued back to back in ONE asm
-// block: the compiler cannot sink them to their uses (it otherwise
-// interleaves load / use to save registers, which leaves one load in flight).
-__device__ __forceinline__ void ldg8(const uint32_t* const (&a)[8], uint32_t (&v)[8]) {
-    asm volatile(
-        "ld.global.nc.u32 %0, [%8];\n\t"
-        "ld.global.nc.u32 %1, [%9];\n\t"
-        "ld.global.nc.u32 %2, [%10];\n\t"
-        "ld.global.nc.u32 %3, [%11];\n\t"
-        "ld.global.nc.u32 %4, [%12];\n\t"
-        "ld.global.nc.u32 %5, [%13];\n\t"
-        "ld.global.nc.u32 %6, [%14];\n\t"
-        "ld.global.nc.u32 %7, [%15];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
-        : "l"(a[0]), "l"(a[1]), "l"(a[2]), "l"(a[3]), "l"(a[4]), "l"(a[5]), "l"(a[6]), "l"(a[7]));
-}
-
-__device__ __forceinline__ void ldg4(const uint32_t* const (&a)[4], uint32_t (&v)[4]) {
-    asm volatile(
-        "ld.global.nc.u32 %0, [%4];\n\t"
-        "ld.global.nc.u32 %1, [%5];\n\t"
-        "ld.global.nc.u32 %2, [%6];\n\t"
-        "ld.global.nc.u32 %3, [%7];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
-        : "l"(a[0]), "l"(a[1]), "l"(a[2]), "l"(a[3]));
 }
 
 // Four predicated 16-byte read-only loads in ONE asm block (all four in
@@ -190,21 +151,5 @@ __device__ __forceinline__ void ldgq(const uint4* const (&a)[4], const bool (&p)
 }
 template <bool NA>
 __device__ __forceinline__ void ldgq(const uint4* const (&a)[2], const bool (&p)[2], uint4 (&v)[2]) { ldg2q(a, p, v); }
-
-// Ampere-style asynchronous 4-byte copies global -> shared (LDGSTS): the
-// data in flight lives in shared memory, not in registers.
-__device__ __forceinline__ void cp_async4(unsigned dst, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-// Multiplicative hash into a power-of-two table of 2^bits slots.
-__device__ __forceinline__ uint32_t slot_hash(uint32_t key, uint32_t shift) {
-    return (key * 0x9E3779B1u) >> shift;  // shift = 32 - bits
-}
 
 }  // namespace trigpu

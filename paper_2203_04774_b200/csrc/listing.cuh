@@ -55,8 +55,8 @@ struct ListParams {
     unsigned int* queue;      // dynamic work counter
     uint32_t* bitmaps;        // class G only: one n-bit bitmap per CTA
     uint64_t bitmap_words;
-    int variant;              // TRIGPU_VARIANT: 2 = null probe (timing experiments only)
-    uint32_t bm_shrink;       // TRIGPU_BM_SHRINK: smaller windows (tests force the below-window path)
+    int variant;              // TL_DEBUG_VARIANT: 2 = null probe (experiments build, timing only)
+    uint32_t bm_shrink;       // TL_DEBUG_BM_SHRINK: smaller windows (tests force the below-window path)
 };
 
 // Per-warp hit buffer (per-vertex-count and list sinks): hits (x, y) are
@@ -186,7 +186,7 @@ struct BitmapProbe {
     __device__ __forceinline__ uint32_t sentinel() const { return n; }
 };
 
-// Timing-only probe (TRIGPU_VARIANT=2 in a -DTRIGPU_EXPERIMENTS build):
+// Timing-only probe (TL_DEBUG_VARIANT 2 in a -DTRIGPU_EXPERIMENTS build):
 // touches every loaded element, never hits. Measures the row-streaming limit.
 struct NullProbe {
     static constexpr bool low = false;

@@ -37,6 +37,22 @@ __global__ void k_inverse(uint32_t n, const uint32_t* __restrict__ rank, uint32_
     }
 }
 
+// Graph CSR offsets: offsets[0] == 0, non-decreasing, offsets[n] == 2m
+// (graph.hpp:20-62). Flag 8 in *err otherwise; checked before any kernel
+// indexes the adjacency through them.
+__global__ void k_check_offsets(uint32_t n, uint64_t m2, const uint64_t* __restrict__ off,
+                                unsigned long long* err) {
+    bool bad = false;
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v <= n;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t o = off[v];
+        if (v == 0) bad |= o != 0;
+        else bad |= off[v - 1] > o;
+        if (v == n) bad |= o != m2;
+    }
+    if (bad) atomicOr(err, 8ull);
+}
+
 // Rows of one warp: 32 consecutive dense rows, one per lane. Rows of fewer
 // than kLongDeg edges are compacted to the low lanes and walked as ONE
 // flattened stream (lane f of a 32-wide window takes element f of the
@@ -400,10 +416,11 @@ __global__ void __launch_bounds__(kLongThreads) k_scatter_long(const uint64_t* _
 // cost_report(view) (cost.cpp:27-38) from the rank-space degree arrays.
 __global__ void __launch_bounds__(256) k_cost(uint32_t n, const uint32_t* __restrict__ outdeg,
                                               const uint32_t* __restrict__ indeg,
-                                              unsigned long long* __restrict__ cost) {
+                                              unsigned long long* __restrict__ cost,
+                                              unsigned long long* __restrict__ sum_out) {
     using BR = cub::BlockReduce<unsigned long long, 256>;
     __shared__ typename BR::TempStorage tmp;
-    unsigned long long pp = 0, pm = 0, mm = 0, dd = 0;
+    unsigned long long pp = 0, pm = 0, mm = 0, dd = 0, so = 0;
     for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n;
          r += (uint64_t)gridDim.x * blockDim.x) {
         const unsigned long long o = outdeg[r], i = indeg[r];
@@ -411,6 +428,7 @@ __global__ void __launch_bounds__(256) k_cost(uint32_t n, const uint32_t* __rest
         pm += o * i;
         mm += i * i;
         dd += (o + i) * (o + i);
+        so += o;
     }
     unsigned long long s;
     s = BR(tmp).Sum(pp);
@@ -424,6 +442,9 @@ __global__ void __launch_bounds__(256) k_cost(uint32_t n, const uint32_t* __rest
     __syncthreads();
     s = BR(tmp).Sum(dd);
     if (threadIdx.x == 0) atomicAdd(&cost[3], s);
+    __syncthreads();
+    s = BR(tmp).Sum(so);  // = m for a symmetric adjacency (checked on the host)
+    if (threadIdx.x == 0) atomicAdd(sum_out, s);
 }
 
 // max over rows of the out-degree (listing batch arithmetic is 32-bit).

@@ -49,10 +49,16 @@ enum Phase {
     PH_IN_CSR,
     PH_CLASSIFY,
     PH_LIST,
+    PH_LIST_R,  // per seed class (the last pass of the last tl_list); G runs on the side stream
+    PH_LIST_H,
+    PH_LIST_C1,
+    PH_LIST_C2,
+    PH_LIST_G,
     PH_COUNT
 };
-const char* kPhaseNames[PH_COUNT] = {"h2d",  "relabel_count", "scan",     "scatter", "segsort",
-                                     "cost", "in_csr",        "classify", "list"};
+const char* kPhaseNames[PH_COUNT] = {"h2d",    "relabel_count", "scan",    "scatter", "segsort", "cost",
+                                     "in_csr", "classify",      "list",    "list_R",  "list_H",  "list_C1",
+                                     "list_C2", "list_G"};
 
 struct DevBuf {
     void* p = nullptr;
@@ -68,6 +74,8 @@ struct tl_ctx {
     cudaEvent_t ev[2 * PH_COUNT + 8] = {};
     cudaEvent_t timer0 = nullptr, timer1 = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
+    cudaEvent_t cls_ev[10] = {};  // start / end of each seed-class launch
+    bool cls_run[5] = {};
     std::string err;
     double phase_ms[PH_COUNT] = {};
     uint64_t launches = 0, orient_launches = 0;
@@ -75,7 +83,8 @@ struct tl_ctx {
     uint32_t n = 0;
     uint64_t m = 0;
     bool oriented = false, in_built = false, hv_built = false;
-    bool normalized = false;  // goff / gadj / labels hold a tl_normalize result
+    bool normalized = false;       // goff / gadj / labels hold a tl_normalize result
+    bool view_normalized = false;  // the oriented view was built from that graph (labels apply)
     uint32_t norm_n = 0;
     uint64_t norm_m = 0;
     uint32_t max_out = 0;
@@ -85,8 +94,8 @@ struct tl_ctx {
     DevBuf goff, gadj, rank, inv, hv, sort_tmp, labels, radj, out_off, out_adj, in_off, in_adj, outdeg, indeg, lists, acc,
         vcount, tri, scan_part, bitmaps, small;
     bool have_vcounts = false, have_tri = false;
-    int variant = 0;         // probe flavour (TRIGPU_VARIANT), for A/B measurement
-    uint32_t bm_shrink = 0;  // TRIGPU_BM_SHRINK: smaller bitmaps (tests force the filter path)
+    int variant = 0;         // TL_DEBUG_VARIANT: probe flavour of an experiments build (A/B timing)
+    uint32_t bm_shrink = 0;  // TL_DEBUG_BM_SHRINK: smaller bitmaps (tests force the filter path)
     unsigned long long tri_count = 0;
 
     tl_status fail(tl_status st, const std::string& what) {
@@ -200,13 +209,21 @@ tl_status sort_rows(tl_ctx* ctx, uint32_t n, uint64_t* off, const uint32_t* len,
     return TL_OK;
 }
 
+// Results of the last tl_list refer to the current view and pi; anything that
+// replaces either drops them.
+void drop_results(tl_ctx* ctx) {
+    ctx->have_vcounts = false;
+    ctx->have_tri = false;
+    ctx->tri_count = 0;
+}
+
 tl_status orient_core(tl_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* goff, const uint32_t* gadj,
                       const uint32_t* rank) {
     ctx->oriented = false;
     ctx->in_built = false;
     ctx->hv_built = false;
-    ctx->have_vcounts = false;
-    ctx->have_tri = false;
+    ctx->view_normalized = false;
+    drop_results(ctx);
     ctx->n = n;
     ctx->m = m;
     ENSURE(inv, (size_t)n * 4);
@@ -227,8 +244,16 @@ tl_status orient_core(tl_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* goff,
     auto* long_cnt = reinterpret_cast<unsigned int*>(flags + 8);  // [0] count, [1] [2] queues
     CK(cudaMemsetAsync(long_cnt, 0, 16, ctx->s));
     if (n) {
+        // pi and the offsets are validated before anything is indexed through them
         k_inverse<<<grid_for(n, 256, big), 256, 0, ctx->s>>>(n, rank, P<uint32_t>(ctx->inv), flags);
         LAUNCHED();
+        k_check_offsets<<<grid_for((uint64_t)n + 1, 256, big), 256, 0, ctx->s>>>(n, 2 * m, goff, flags);
+        LAUNCHED();
+        unsigned long long pre = 0;
+        CK(cudaMemcpyAsync(&pre, flags, 8, cudaMemcpyDeviceToHost, ctx->s));
+        CK(cudaStreamSynchronize(ctx->s));
+        if (pre & 3ull) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "orient: ordering does not match graph (rank is not a permutation of [0, n))");
+        if (pre & 8ull) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "orient: offsets must start at 0, be non-decreasing and end at 2m");
         k_relabel_count<<<grid_for((uint64_t)n, 256, big * 2), 256, 0, ctx->s>>>(
             n, goff, gadj, rank, P<uint32_t>(ctx->radj), P<uint32_t>(ctx->outdeg), P<uint32_t>(ctx->indeg),
             long_rows, long_cnt, flags);
@@ -257,6 +282,9 @@ tl_status orient_core(tl_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* goff,
     if (errflag & 4ull) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "orient: adjacency violates the Graph invariants (rows must be strictly increasing, in range, loop-free)");
     if (padded / 4 >= (1ull << 32)) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "orient: graph too large (> 2^32 quads of out-rows)");
     ENSURE(out_adj, padded * 4 + 64);
+    // radj becomes the big-row sort's temp row, indexed by the PADDED offsets
+    // (up to m + 3n slots): grow it now, its contents are dead after k_scatter
+    const size_t radj_need = std::max<size_t>(2 * m, padded + 64) * 4;
     if (n) {
         k_scatter<<<grid_for((uint64_t)n, 256, big * 2), 256, 0, ctx->s>>>(
             n, goff, P<uint32_t>(ctx->radj), rank, P<uint64_t>(ctx->out_off), P<uint32_t>(ctx->outdeg),
@@ -269,24 +297,30 @@ tl_status orient_core(tl_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* goff,
         LAUNCHED();
     }
     CK(cudaEventRecord(ctx->ev[PH_SCATTER], ctx->s));
+    if (ctx->radj.cap < radj_need) {
+        CK(cudaStreamSynchronize(ctx->s));  // k_scatter still reads radj
+        ENSURE(radj, radj_need);
+    }
     st = sort_rows(ctx, n, P<uint64_t>(ctx->out_off), P<uint32_t>(ctx->outdeg), P<uint32_t>(ctx->out_adj),
                    P<uint32_t>(ctx->radj));
     if (st != TL_OK) return st;
     CK(cudaEventRecord(ctx->ev[PH_SORT], ctx->s));
     // costs + max out-degree
-    CK(cudaMemsetAsync(flags + 2, 0, 5 * 8, ctx->s));
+    CK(cudaMemsetAsync(flags + 2, 0, 6 * 8, ctx->s));
     if (n) {
         k_cost<<<grid_for(n, 256, ctx->sms * 4), 256, 0, ctx->s>>>(n, P<uint32_t>(ctx->outdeg), P<uint32_t>(ctx->indeg),
-                                                                  flags + 2);
+                                                                  flags + 2, flags + 7);
         LAUNCHED();
         k_maxdeg<<<grid_for(n, 256, ctx->sms * 4), 256, 0, ctx->s>>>(n, P<uint32_t>(ctx->outdeg),
                                                                     reinterpret_cast<unsigned int*>(flags + 6));
         LAUNCHED();
     }
     CK(cudaEventRecord(ctx->ev[PH_COST], ctx->s));
-    unsigned long long res[5];
+    unsigned long long res[6];
     CK(cudaMemcpyAsync(res, flags + 2, sizeof(res), cudaMemcpyDeviceToHost, ctx->s));
     CK(cudaStreamSynchronize(ctx->s));
+    if (res[5] != m)  // each undirected edge oriented once: only if every (u, v) has its (v, u) (graph.cpp:108)
+        return ctx->fail(TL_ERR_INVALID_ARGUMENT, "orient: adjacency is not symmetric (out-degrees do not sum to m)");
     std::memcpy(ctx->cost, res, sizeof(ctx->cost));
     ctx->max_out = static_cast<uint32_t>(res[4]);
     ctx->phase_ms[PH_RELABEL] = ev_ms(ctx->ev[PH_H2D], ctx->ev[PH_RELABEL]);
@@ -301,16 +335,22 @@ tl_status orient_core(tl_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* goff,
 }
 
 // k_transpose: in-row s receives r for every successor s of r.
+// Writes are bounded by the in-row's end (in_off[s + 1]): an asymmetric
+// adjacency that slipped past the degree-sum check sets *err instead of
+// writing past the row.
 __global__ void k_transpose(uint32_t n, const uint64_t* __restrict__ out_off, const uint32_t* __restrict__ outdeg,
                             const uint32_t* __restrict__ out_adj, unsigned long long* __restrict__ cursor,
-                            uint32_t* __restrict__ in_adj) {
+                            const uint64_t* __restrict__ in_off, uint32_t* __restrict__ in_adj,
+                            unsigned long long* __restrict__ err) {
     const unsigned lane = lane_id();
     const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t r = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; r < n; r += warps) {
         const uint64_t b = out_off[r], e = b + outdeg[r];
         for (uint64_t i = b + lane; i < e; i += 32) {
             const uint32_t s = out_adj[i];
-            in_adj[atomicAdd(&cursor[s], 1ull)] = static_cast<uint32_t>(r);
+            const unsigned long long pos = atomicAdd(&cursor[s], 1ull);
+            if (pos < in_off[s + 1]) in_adj[pos] = static_cast<uint32_t>(r);
+            else atomicOr(err, 16ull);
         }
     }
 }
@@ -332,10 +372,17 @@ tl_status ensure_in_csr(tl_ctx* ctx) {
     auto* cursor = P<unsigned long long>(ctx->radj);
     if (n) {
         CK(cudaMemcpyAsync(cursor, ctx->in_off.p, (size_t)n * 8, cudaMemcpyDeviceToDevice, ctx->s));
+        ENSURE(small, 128);
+        auto* flags = static_cast<unsigned long long*>(ctx->small.p);
+        CK(cudaMemsetAsync(flags, 0, 8, ctx->s));
         k_transpose<<<grid_for((uint64_t)n * 32, 256, ctx->sms * 32), 256, 0, ctx->s>>>(
             n, P<uint64_t>(ctx->out_off), P<uint32_t>(ctx->outdeg), P<uint32_t>(ctx->out_adj), cursor,
-            P<uint32_t>(ctx->in_adj));
+            P<uint64_t>(ctx->in_off), P<uint32_t>(ctx->in_adj), flags);
         LAUNCHED();
+        unsigned long long err = 0;
+        CK(cudaMemcpyAsync(&err, flags, 8, cudaMemcpyDeviceToHost, ctx->s));
+        CK(cudaStreamSynchronize(ctx->s));
+        if (err) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "orient: adjacency is not symmetric (in-rows overflow)");
     }
     st = sort_rows(ctx, n, P<uint64_t>(ctx->in_off), nullptr, P<uint32_t>(ctx->in_adj), P<uint32_t>(ctx->radj));
     if (st != TL_OK) return st;
@@ -399,9 +446,12 @@ tl_status launch_classes(tl_ctx* ctx, ListParams base, uint32_t* const lists[kCl
         p.bitmaps = P<uint32_t>(ctx->bitmaps);
         CK(cudaEventRecord(ctx->fork, ctx->s));
         CK(cudaStreamWaitEvent(ctx->s2, ctx->fork, 0));
+        CK(cudaEventRecord(ctx->cls_ev[8], ctx->s2));
         k_list_giant<ALGO, F><<<grid, kGThreads, smem, ctx->s2>>>(p);
         LAUNCHED();
+        CK(cudaEventRecord(ctx->cls_ev[9], ctx->s2));
         CK(cudaEventRecord(ctx->join, ctx->s2));
+        ctx->cls_run[4] = true;
     }
     if (h[0]) {
         ListParams p = base;
@@ -412,8 +462,11 @@ tl_status launch_classes(tl_ctx* ctx, ListParams base, uint32_t* const lists[kCl
         if ((st = set_smem(ctx, k_list_reg<ALGO, F>, smem)) != TL_OK) return st;
         const unsigned grid = std::min<unsigned>(grid_for((uint64_t)h[0] * 32, kRWarps * 32, ~0u),
                                                  resident_grid(ctx, k_list_reg<ALGO, F>, kRWarps * 32, smem));
+        CK(cudaEventRecord(ctx->cls_ev[0], ctx->s));
         k_list_reg<ALGO, F><<<grid, kRWarps * 32, smem, ctx->s>>>(p);
         LAUNCHED();
+        CK(cudaEventRecord(ctx->cls_ev[1], ctx->s));
+        ctx->cls_run[0] = true;
     }
     if (h[1]) {
         ListParams p = base;
@@ -424,16 +477,25 @@ tl_status launch_classes(tl_ctx* ctx, ListParams base, uint32_t* const lists[kCl
         if ((st = set_smem(ctx, k_list_warp<ALGO, F>, smem)) != TL_OK) return st;
         const unsigned grid = std::min<unsigned>(grid_for((uint64_t)h[1] * 32, kHWarps * 32, ~0u),
                                                  resident_grid(ctx, k_list_warp<ALGO, F>, kHWarps * 32, smem));
+        CK(cudaEventRecord(ctx->cls_ev[2], ctx->s));
         k_list_warp<ALGO, F><<<grid, kHWarps * 32, smem, ctx->s>>>(p);
         LAUNCHED();
+        CK(cudaEventRecord(ctx->cls_ev[3], ctx->s));
+        ctx->cls_run[1] = true;
     }
     if (h[2]) {
+        CK(cudaEventRecord(ctx->cls_ev[4], ctx->s));
         st = launch_cta<ALGO, F, CfgC1>(ctx, base, lists[2], h[2], queues + 2);
         if (st != TL_OK) return st;
+        CK(cudaEventRecord(ctx->cls_ev[5], ctx->s));
+        ctx->cls_run[2] = true;
     }
     if (h[3]) {
+        CK(cudaEventRecord(ctx->cls_ev[6], ctx->s));
         st = launch_cta<ALGO, F, CfgC2>(ctx, base, lists[3], h[3], queues + 3);
         if (st != TL_OK) return st;
+        CK(cudaEventRecord(ctx->cls_ev[7], ctx->s));
+        ctx->cls_run[3] = true;
     }
     if (h[4]) CK(cudaStreamWaitEvent(ctx->s, ctx->join, 0));
     return TL_OK;
@@ -484,8 +546,6 @@ TL_API tl_status tl_create(tl_ctx** out, int device) {
     tl_ctx* ctx = new tl_ctx();
     ctx->device = device;
     ctx->sms = prop.multiProcessorCount;
-    if (const char* v = std::getenv("TRIGPU_VARIANT")) ctx->variant = std::atoi(v);
-    if (const char* v = std::getenv("TRIGPU_BM_SHRINK")) ctx->bm_shrink = (uint32_t)std::atoi(v);
     if ((e = cudaSetDevice(device)) != cudaSuccess || (e = cudaStreamCreateWithFlags(&ctx->s, cudaStreamNonBlocking)) != cudaSuccess ||
         (e = cudaStreamCreateWithFlags(&ctx->s2, cudaStreamNonBlocking)) != cudaSuccess) {
         g_create_error = std::string("tl_create: ") + cudaGetErrorString(e);
@@ -493,6 +553,7 @@ TL_API tl_status tl_create(tl_ctx** out, int device) {
         return TL_ERR_CUDA;
     }
     for (auto& ev : ctx->ev) cudaEventCreate(&ev);
+    for (auto& ev : ctx->cls_ev) cudaEventCreate(&ev);
     cudaEventCreateWithFlags(&ctx->fork, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ctx->join, cudaEventDisableTiming);
     *out = ctx;
@@ -511,6 +572,7 @@ TL_API void tl_destroy(tl_ctx* ctx) {
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     for (auto& ev : ctx->ev) cudaEventDestroy(ev);
+    for (auto& ev : ctx->cls_ev) cudaEventDestroy(ev);
     if (ctx->timer0) cudaEventDestroy(ctx->timer0);
     if (ctx->timer1) cudaEventDestroy(ctx->timer1);
     cudaEventDestroy(ctx->fork);
@@ -528,10 +590,12 @@ TL_API tl_status tl_check_sizes(uint32_t graph_n, uint32_t rank_n) {
     return graph_n == rank_n ? TL_OK : TL_ERR_INVALID_ARGUMENT;
 }
 
-static tl_status check_args(tl_ctx* ctx, uint32_t n, uint64_t m, const void* off, const void* adj, const void* rank) {
+static tl_status check_args(tl_ctx* ctx, uint32_t n, uint64_t m, const void* off, const void* adj, const void* rank,
+                            bool need_rank = true) {
     if (!ctx) return TL_ERR_INVALID_ARGUMENT;
     ctx->launches = 0;
-    if ((n && (!off || !rank)) || (m && !adj)) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "orient: null input pointer");
+    if ((n && (!off || (need_rank && !rank))) || (m && !adj))
+        return ctx->fail(TL_ERR_INVALID_ARGUMENT, "orient: null input pointer");
     if (n == 0xFFFFFFFFu) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "orient: n must be < 2^32 - 1 (VertexId, common.hpp:11-13)");
     if (n > 0xFFF00000u)  // the listing pads partial quads with kNone, which must lie 2^20 above every rank
         return ctx->fail(TL_ERR_INVALID_ARGUMENT, "orient: n > 2^32 - 2^20 is not supported by the listing engine");
@@ -546,6 +610,7 @@ TL_API tl_status tl_orient(tl_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* 
     if (st != TL_OK) return st;
     if (n && offsets[0] != 0) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "orient: offsets[0] must be 0");
     if (n && offsets[n] != 2 * m) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "orient: offsets[n] must equal 2m");
+    ctx->normalized = false;  // goff / gadj are overwritten
     ENSURE(goff, ((size_t)n + 1) * 8);
     ENSURE(gadj, 2 * m * 4);
     ENSURE(rank, (size_t)n * 4);
@@ -597,6 +662,10 @@ TL_API tl_status tl_order(tl_ctx* ctx, uint32_t n, const uint64_t* offsets, int 
     if (!ctx || (n && (!offsets || !rank))) return TL_ERR_INVALID_ARGUMENT;
     if (n == 0xFFFFFFFFu) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "order: n must be < 2^32 - 1");
     if (cudaSetDevice(ctx->device) != cudaSuccess) return ctx->cuda_fail("cudaSetDevice", cudaGetLastError());
+    // goff and rank are overwritten: the view, its results and a normalized graph go
+    ctx->normalized = false;
+    ctx->oriented = false;
+    drop_results(ctx);
     ENSURE(goff, ((size_t)n + 1) * 8);
     ENSURE(rank, (size_t)n * 4 + 4);
     CK(cudaMemcpyAsync(ctx->goff.p, offsets, ((size_t)n + 1) * 8, cudaMemcpyHostToDevice, ctx->s));
@@ -604,24 +673,23 @@ TL_API tl_status tl_order(tl_ctx* ctx, uint32_t n, const uint64_t* offsets, int 
     if (st != TL_OK) return st;
     if (n) CK(cudaMemcpyAsync(rank, ctx->rank.p, (size_t)n * 4, cudaMemcpyDeviceToHost, ctx->s));
     CK(cudaStreamSynchronize(ctx->s));
-    ctx->oriented = false;  // the owned rank / offsets copies were overwritten
     return TL_OK;
 }
 
 TL_API tl_status tl_orient_ordered(tl_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* offsets, const uint32_t* adj,
                                    int method) {
-    if (!ctx || (n && !offsets) || (m && !adj)) return TL_ERR_INVALID_ARGUMENT;
-    if (cudaSetDevice(ctx->device) != cudaSuccess) return ctx->cuda_fail("cudaSetDevice", cudaGetLastError());
-    if (n == 0xFFFFFFFFu) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "orient: n must be < 2^32 - 1 (VertexId, common.hpp:11-13)");
+    tl_status st = check_args(ctx, n, m, offsets, adj, nullptr, false);
+    if (st != TL_OK) return st;
     if (n && offsets[0] != 0) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "orient: offsets[0] must be 0");
     if (n && offsets[n] != 2 * m) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "orient: offsets[n] must equal 2m");
+    ctx->normalized = false;  // goff / gadj are overwritten
     ENSURE(goff, ((size_t)n + 1) * 8);
     ENSURE(gadj, 2 * m * 4);
     ENSURE(rank, (size_t)n * 4 + 4);
     CK(cudaEventRecord(ctx->ev[PH_COUNT + 2], ctx->s));
     CK(cudaMemcpyAsync(ctx->goff.p, offsets, ((size_t)n + 1) * 8, cudaMemcpyHostToDevice, ctx->s));
     if (m) CK(cudaMemcpyAsync(ctx->gadj.p, adj, 2 * m * 4, cudaMemcpyHostToDevice, ctx->s));
-    tl_status st = order_core(ctx, n, P<uint64_t>(ctx->goff), method, P<uint32_t>(ctx->rank));
+    st = order_core(ctx, n, P<uint64_t>(ctx->goff), method, P<uint32_t>(ctx->rank));
     if (st != TL_OK) return st;
     CK(cudaEventRecord(ctx->ev[PH_H2D], ctx->s));
     st = orient_core(ctx, n, m, P<uint64_t>(ctx->goff), P<uint32_t>(ctx->gadj), P<uint32_t>(ctx->rank));
@@ -636,8 +704,9 @@ TL_API tl_status tl_normalize(tl_ctx* ctx, uint64_t k, const int64_t* edges, uin
     if (!ctx || (k && !edges) || !n_out || !m_out) return TL_ERR_INVALID_ARGUMENT;
     if (cudaSetDevice(ctx->device) != cudaSuccess) return ctx->cuda_fail("cudaSetDevice", cudaGetLastError());
     ctx->normalized = false;
-    ctx->oriented = false;
-    if (k >= (1ull << 31)) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "normalize: more than 2^31 - 1 raw edges");
+    ctx->oriented = false;  // goff / gadj / outdeg / radj are reused below
+    drop_results(ctx);
+    if (k >= (1ull << 30)) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "normalize: more than 2^30 - 1 raw edges");
     // scratch: raw (2k) | a, b (k each) | a2, b2 (k each) in radj-sized buffers
     ENSURE(radj, std::max<size_t>(k * 16 * 3 + 64, 64));
     ENSURE(small, 128);
@@ -765,16 +834,17 @@ TL_API tl_status tl_fetch_graph(tl_ctx* ctx, uint64_t* offsets, uint32_t* adj, i
 TL_API tl_status tl_orient_normalized(tl_ctx* ctx, int method) {
     if (!ctx) return TL_ERR_INVALID_ARGUMENT;
     if (!ctx->normalized) return ctx->fail(TL_ERR_STATE, "tl_orient_normalized: no normalized graph (call tl_normalize)");
-    if (cudaSetDevice(ctx->device) != cudaSuccess) return ctx->cuda_fail("cudaSetDevice", cudaGetLastError());
     const uint32_t n = ctx->norm_n;
+    tl_status st = check_args(ctx, n, ctx->norm_m, ctx->goff.p, ctx->gadj.p, nullptr, false);
+    if (st != TL_OK) return st;
     ENSURE(rank, (size_t)n * 4 + 4);
-    tl_status st = order_core(ctx, n, P<uint64_t>(ctx->goff), method, P<uint32_t>(ctx->rank));
+    st = order_core(ctx, n, P<uint64_t>(ctx->goff), method, P<uint32_t>(ctx->rank));
     if (st != TL_OK) return st;
     CK(cudaEventRecord(ctx->ev[PH_H2D], ctx->s));
     st = orient_core(ctx, n, ctx->norm_m, P<uint64_t>(ctx->goff), P<uint32_t>(ctx->gadj), P<uint32_t>(ctx->rank));
     if (st != TL_OK) return st;
     ctx->h2d_ms = ctx->phase_ms[PH_H2D] = 0;
-    ctx->normalized = true;  // goff / gadj untouched by orientation
+    ctx->view_normalized = true;  // goff / gadj / labels untouched by orientation
     return TL_OK;
 }
 
@@ -866,6 +936,7 @@ TL_API tl_status tl_list(tl_ctx* ctx, int algo, unsigned out_flags, tl_stats* ou
 
     CK(cudaEventRecord(ctx->ev[PH_COUNT + 4], ctx->s));  // listing kernels start
     auto run = [&](unsigned F) -> tl_status {
+        for (bool& r : ctx->cls_run) r = false;
         CK(cudaMemsetAsync(acc, 0, 8 * sizeof(unsigned long long), ctx->s));
         CK(cudaMemsetAsync(counts + 8, 0, 8 * sizeof(unsigned int), ctx->s));
         if (F & F_VCOUNT) CK(cudaMemsetAsync(ctx->vcount.p, 0, (size_t)n * 8, ctx->s));
@@ -890,6 +961,8 @@ TL_API tl_status tl_list(tl_ctx* ctx, int algo, unsigned out_flags, tl_stats* ou
     CK(cudaStreamSynchronize(ctx->s));
     ctx->phase_ms[PH_CLASSIFY] = ev_ms(ctx->ev[PH_COUNT + 3], ctx->ev[PH_CLASSIFY]);
     ctx->phase_ms[PH_LIST] = ev_ms(ctx->ev[PH_COUNT + 4], ctx->ev[PH_LIST]);
+    for (int c = 0; c < kClasses; ++c)
+        ctx->phase_ms[PH_LIST_R + c] = ctx->cls_run[c] ? ev_ms(ctx->cls_ev[2 * c], ctx->cls_ev[2 * c + 1]) : 0.0;
     ctx->have_vcounts = want_vc;
     ctx->have_tri = want_list;
     ctx->tri_count = want_list ? res[2] : 0;
@@ -943,7 +1016,7 @@ TL_API tl_status tl_fetch_triangle_labels(tl_ctx* ctx, uint64_t first, uint64_t 
                                           int64_t* out, uint64_t* k) {
     if (!ctx || !k) return TL_ERR_INVALID_ARGUMENT;
     if (!ctx->have_tri) return ctx->fail(TL_ERR_STATE, "tl_fetch_triangle_labels: last tl_list did not use TL_OUT_LIST");
-    if (!labels && !(ctx->normalized && ctx->norm_n == ctx->n))
+    if (!labels && !(ctx->normalized && ctx->view_normalized))
         return ctx->fail(TL_ERR_STATE, "tl_fetch_triangle_labels: no label table (pass one, or orient a tl_normalize graph)");
     if (cudaSetDevice(ctx->device) != cudaSuccess) return ctx->cuda_fail("cudaSetDevice", cudaGetLastError());
     *k = first < ctx->tri_count ? std::min<uint64_t>(cap, ctx->tri_count - first) : 0;
@@ -953,8 +1026,7 @@ TL_API tl_status tl_fetch_triangle_labels(tl_ctx* ctx, uint64_t first, uint64_t 
     if (labels) {  // caller's table: stage it after the normalize labels' slot
         ENSURE(sort_tmp, (size_t)ctx->n * 8 + 64);
         CK(cudaMemcpyAsync(ctx->sort_tmp.p, labels, (size_t)ctx->n * 8, cudaMemcpyHostToDevice, ctx->s));
-        lab = P<long long>(ctx->sort_tmp);
-        ctx->normalized = false;  // sort_tmp is normalize's scratch; the graph itself stays valid
+        lab = P<long long>(ctx->sort_tmp);  // normalize's scratch; its graph and labels stay valid
     }
     ENSURE(scan_part, *k * 24);
     k_map_labels<<<grid_for(*k * 3, 256, ctx->sms * 16), 256, 0, ctx->s>>>(*k * 3, P<uint32_t>(ctx->tri) + 3 * first, lab,
@@ -1088,5 +1160,19 @@ TL_API int tl_phase_times(const tl_ctx* ctx, double* ms, int cap) {
 }
 
 TL_API const char* tl_phase_name(int i) { return (i >= 0 && i < PH_COUNT) ? kPhaseNames[i] : ""; }
+
+TL_API tl_status tl_debug_set(tl_ctx* ctx, int key, int value) {
+    if (!ctx || value < 0) return TL_ERR_INVALID_ARGUMENT;
+    if (key == TL_DEBUG_BM_SHRINK) {
+        if (value > 16) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "tl_debug_set: shrink must be <= 16");
+        ctx->bm_shrink = static_cast<uint32_t>(value);
+        return TL_OK;
+    }
+    if (key == TL_DEBUG_VARIANT) {
+        ctx->variant = value;
+        return TL_OK;
+    }
+    return ctx->fail(TL_ERR_INVALID_ARGUMENT, "tl_debug_set: unknown key");
+}
 
 }  // extern "C"

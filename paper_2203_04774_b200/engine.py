@@ -209,6 +209,10 @@ class Context:
         _check(self._p, _native.trigpu().tl_timer_stop(self._p, C.byref(ms)))
         return ms.value
 
+    def debug_set(self, key: int, value: int) -> None:
+        """Test-only knobs (tl_debug_set): TL_DEBUG_BM_SHRINK, TL_DEBUG_VARIANT."""
+        _check(self._p, _native.trigpu().tl_debug_set(self._p, key, value))
+
     def phase_times(self) -> dict:
         lib = _native.trigpu()
         buf = (C.c_double * 32)()

@@ -12,8 +12,8 @@ import pytest
 import oracle
 import paper_2203_04774_b200 as tg
 from paper_2203_04774_b200 import host
-from paper_2203_04774_b200._native import (TL_ALGO_APM, TL_ALGO_APP, TL_OUT_CHECKSUM, TL_OUT_LIST,
-                                           TL_OUT_VERTEX_COUNTS)
+from paper_2203_04774_b200._native import (TL_ALGO_APM, TL_ALGO_APP, TL_DEBUG_BM_SHRINK, TL_OUT_CHECKSUM,
+                                           TL_OUT_LIST, TL_OUT_VERTEX_COUNTS)
 from golden_io import case_csr, cases, golden, sha, sweep_graphs
 
 pytestmark = pytest.mark.gpu
@@ -267,14 +267,14 @@ def test_full_size_c4_properties(ctx):
 
 
 @pytest.mark.parametrize("shrink", [4, 8, 13])
-def test_probe_filter_path(monkeypatch, shrink):
+def test_probe_filter_path(shrink):
     """Each seed's set is a windowed bitmap: exact when the set's rank span
     fits, otherwise a filter whose candidates are verified exactly.
-    Shrinking every class's bitmap (TRIGPU_BM_SHRINK) pushes the seeds of
+    Shrinking every class's bitmap (tl_debug_set TL_DEBUG_BM_SHRINK) pushes the seeds of
     graphs small enough for the oracle through the filter + verification path
     with many false positives; results must not change."""
-    monkeypatch.setenv("TRIGPU_BM_SHRINK", str(shrink))
     c = tg.Context(0)
+    c.debug_set(TL_DEBUG_BM_SHRINK, shrink)
     try:
         for g in (tg.gen_rmat(15, 16, 3), tg.gen_chung_lu(50000, 800000, seed=4)):
             for meth in ("degree", "split"):
