@@ -41,6 +41,12 @@ $(LIB)/libtrigpu_exp.so: $(CU_SRCS) $(CU_HDRS)
 	@mkdir -p $(LIB)
 	$(NVCC) $(NVFLAGS) -DTRIGPU_EXPERIMENTS -shared $(CU_SRCS) -o $@ -lcudart_static -lrt -ldl -lpthread
 
+# tuning variants for A/B timing: make gpu_var VAR=_x DEFS="-DTRIGPU_C1_RING=4"
+# (select with TRIGPU_LIB_SUFFIX=_x)
+gpu_var:
+	@mkdir -p $(LIB)
+	$(NVCC) $(NVFLAGS) $(DEFS) -Xptxas -v -shared $(CU_SRCS) -o $(LIB)/libtrigpu$(VAR).so -lcudart_static -lrt -ldl -lpthread 2> build_ptxas$(VAR).log || (cat build_ptxas$(VAR).log; exit 1)
+
 $(LIB)/libtrihost.so: $(CSRC)/host/trihost.cpp $(CSRC)/host/trihost.h $(REF_HOST_SRCS)
 	@mkdir -p $(LIB)
 	$(CXX) -std=c++20 -O3 -fPIC -shared -I$(REF)/core/include -I$(CSRC)/host \
@@ -59,4 +65,4 @@ clean:
 	rm -rf $(LIB)/*.so build
 	$(MAKE) -C oracle clean
 
-.PHONY: all gpu host oracle clean
+.PHONY: all gpu host oracle clean gpu_var

@@ -127,6 +127,13 @@ TL_API tl_status tl_check_sizes(uint32_t graph_n, uint32_t rank_n);
 /* List every triangle once over G_pi with A++ (TL_ALGO_APP, listing.hpp:69-86)
  * or A+- (TL_ALGO_APM, listing.hpp:91-107). */
 TL_API tl_status tl_list(tl_ctx* ctx, int algo, unsigned out_flags, tl_stats* out);
+/* tl_list restricted to the seeds whose rank lies in [rank_begin, rank_end):
+ * detail::run_app_range / run_apm_range (listing.hpp:69-107) over one rank
+ * range, the unit run_parallel hands its lanes (listing.hpp:122-155).
+ * inner_ops / mark_ops count that range's seeds only (c_pm / c_pp and 2m
+ * over the full range); every sink is supported. */
+TL_API tl_status tl_list_range(tl_ctx* ctx, int algo, unsigned out_flags, uint32_t rank_begin,
+                               uint32_t rank_end, tl_stats* out);
 
 /* Copy the triangles of the last TL_OUT_LIST run: 3*k dense ids, each triple
  * rank-ascending (u, v, w), triples in unspecified order. cap in triangles.

@@ -59,6 +59,10 @@ def lib() -> C.CDLL:
     L.or_list_ranges.argtypes = [C.c_int, _u32, _vp, _vp, _vp, _vp, _vp, _vp, _u64, C.c_int,
                                  C.POINTER(OrStats)]
     L.or_list_ranges.restype = C.c_int
+    L.or_orient_parallel.argtypes = [_u32, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, C.c_int]
+    L.or_orient_parallel.restype = C.c_int
+    L.or_sort_triples.argtypes = [_vp, _u64, C.c_int]
+    L.or_sort_triples.restype = None
     return L
 
 
@@ -137,8 +141,8 @@ class OrientedCSR:
     rank: np.ndarray
 
 
-def orient(offsets: np.ndarray, adj: np.ndarray, rank: np.ndarray) -> OrientedCSR:
-    """or_orient <- oriented_view.cpp:7-47."""
+def orient(offsets: np.ndarray, adj: np.ndarray, rank: np.ndarray, threads: int = 1) -> OrientedCSR:
+    """or_orient <- oriented_view.cpp:7-47 (threads > 1: or_orient_parallel, same output)."""
     n = offsets.shape[0] - 1
     m = adj.shape[0] // 2
     offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
@@ -151,8 +155,13 @@ def orient(offsets: np.ndarray, adj: np.ndarray, rank: np.ndarray) -> OrientedCS
     s = np.zeros(max(m, 1), np.uint32)
     p = np.zeros(max(m, 1), np.uint32)
     inv = np.zeros(max(n, 1), np.uint32)
-    rc = lib().or_orient(n, m, offsets.ctypes.data, adj.ctypes.data, rank.ctypes.data,
-                         so.ctypes.data, s.ctypes.data, po.ctypes.data, p.ctypes.data, inv.ctypes.data)
+    if threads > 1:
+        rc = lib().or_orient_parallel(n, m, offsets.ctypes.data, adj.ctypes.data, rank.ctypes.data,
+                                      so.ctypes.data, s.ctypes.data, po.ctypes.data, p.ctypes.data,
+                                      inv.ctypes.data, threads)
+    else:
+        rc = lib().or_orient(n, m, offsets.ctypes.data, adj.ctypes.data, rank.ctypes.data,
+                             so.ctypes.data, s.ctypes.data, po.ctypes.data, p.ctypes.data, inv.ctypes.data)
     if rc != 0:
         raise ValueError("orient: ordering does not match graph")
     return OrientedCSR(so, s[:m], po, p[:m], inv[:n], rank)
@@ -229,6 +238,14 @@ def brute(offsets: np.ndarray, adj: np.ndarray) -> np.ndarray:
     out = np.zeros((max(k, 1), 3), np.uint32)
     lib().or_brute(n, offsets.ctypes.data, adj.ctypes.data, out.ctypes.data, k)
     return out[:k]
+
+
+def sort_triples(tri: np.ndarray, threads: int = 1) -> np.ndarray:
+    """CollectingSink::canonical in place on a (k, 3) uint32 array (or_sort_triples)."""
+    assert tri.dtype == np.uint32 and tri.flags["C_CONTIGUOUS"] and tri.ndim == 2 and tri.shape[1] == 3
+    if tri.shape[0]:
+        lib().or_sort_triples(tri.ctypes.data, tri.shape[0], threads)
+    return tri
 
 
 def canonical(tri: np.ndarray) -> np.ndarray:
@@ -368,13 +385,13 @@ class RefView:
         return so, s[: self.m], po, p[: self.m]
 
     def list(self, algo: int, threads: int = 1, vcounts=False, collect=False, rank_begin=0,
-             rank_end=None) -> ListResult:
+             rank_end=None, tri_cap=None) -> ListResult:
         re = self.n if rank_end is None else rank_end
         vc = np.zeros(max(self.n, 1), np.uint64) if vcounts else None
         cap = 0
         tri = None
         if collect:
-            cap = 4 * self.m + 16
+            cap = 4 * self.m + 16 if tri_cap is None else max(int(tri_cap), 1)
             tri = np.zeros((cap, 3), np.uint32)
         k = C.c_uint64(0)
         st = RefStats()

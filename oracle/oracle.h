@@ -61,6 +61,14 @@ uint64_t or_list(int algo, uint32_t n, const uint64_t* succ_off, const uint32_t*
                  uint64_t* vcounts, uint32_t* tri, uint64_t tri_cap, or_stats* out);
 
 /* cost_report(view) (reference cost.cpp:27-38): out = {c_pp, c_pm, c_mm, sum_deg_sq}. */
+/* or_orient with `threads` lanes (bulk.cpp): identical output; for the
+ * full-size parity tests. */
+int or_orient_parallel(uint32_t n, uint64_t m, const uint64_t* offsets, const uint32_t* adj,
+                       const uint32_t* rank, uint64_t* succ_off, uint32_t* succ,
+                       uint64_t* pred_off, uint32_t* pred, uint32_t* inverse, int threads);
+/* CollectingSink::canonical (listing.hpp:57-62) in place over k triples
+ * (sort inside each triple, then the triples), `threads` lanes (bulk.cpp). */
+void or_sort_triples(uint32_t* tri, uint64_t k, int threads);
 /* or_list over a sample of rank ranges [ranges[2i], ranges[2i+1]) in one
  * pulling pass (count + checksum only). */
 int or_list_ranges(int algo, uint32_t n, const uint64_t* succ_off, const uint32_t* succ,

@@ -46,7 +46,7 @@ TRIGPU_SYMBOLS = (
     "tl_host_register", "tl_host_unregister", "tl_phase_times", "tl_phase_name",
     "tl_timer_start", "tl_timer_stop", "tl_order", "tl_order_device", "tl_orient_ordered",
     "tl_fetch_ranks", "tl_normalize", "tl_fetch_graph", "tl_orient_normalized",
-    "tl_fetch_triangles_range", "tl_fetch_triangle_labels", "tl_debug_set",
+    "tl_fetch_triangles_range", "tl_fetch_triangle_labels", "tl_debug_set", "tl_list_range",
 )
 
 
@@ -85,6 +85,14 @@ _u32 = C.c_uint32
 _u64 = C.c_uint64
 
 
+def use_library_variant(suffix: str) -> None:
+    """Switch later trigpu() calls to lib/libtrigpu<suffix>.so (A/B timing of
+    tuning builds, tools/ab.py); contexts created before keep their library."""
+    global TRIGPU_PATH
+    TRIGPU_PATH = os.path.join(LIB_DIR, "libtrigpu%s.so" % suffix)
+    trigpu.cache_clear()
+
+
 @lru_cache(maxsize=None)
 def trigpu() -> C.CDLL:
     if not os.path.exists(TRIGPU_PATH):
@@ -107,6 +115,8 @@ def trigpu() -> C.CDLL:
     lib.tl_check_sizes.restype = C.c_int
     lib.tl_list.argtypes = [_vp, C.c_int, C.c_uint, C.POINTER(TlStats)]
     lib.tl_list.restype = C.c_int
+    lib.tl_list_range.argtypes = [_vp, C.c_int, C.c_uint, C.c_uint32, C.c_uint32, C.POINTER(TlStats)]
+    lib.tl_list_range.restype = C.c_int
     lib.tl_fetch_triangles.argtypes = [_vp, _vp, _u64, C.POINTER(_u64)]
     lib.tl_fetch_triangles.restype = C.c_int
     lib.tl_fetch_vertex_counts.argtypes = [_vp, _vp]

@@ -144,6 +144,73 @@ __device__ __forceinline__ void ldg2q(const uint4* const (&a)[2], const bool (&p
           "+r"(v[1].w)
         : "r"((unsigned)p[0]), "r"((unsigned)p[1]), "l"(a[0]), "l"(a[1]));
 }
+// L2 eviction-priority policies (createpolicy): rows re-read by many seeds
+// are loaded evict_last, the rest evict_first, so the hot rows stay in L2.
+__device__ __forceinline__ uint64_t l2_policy_last() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ uint64_t l2_policy_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+// ldg4q / ldg2q with a per-load L2 policy (NA: no L1 allocation as ldg4q_na)
+template <bool NA>
+__device__ __forceinline__ void ldgq_pol(const uint4* const (&a)[4], const bool (&p)[4], const uint64_t (&pol)[4],
+                                         uint4 (&v)[4]) {
+    if constexpr (NA)
+        asm volatile(
+            "{\n\t.reg .pred q0, q1, q2, q3;\n\t"
+            "setp.ne.u32 q0, %16, 0;\n\t"
+            "setp.ne.u32 q1, %17, 0;\n\t"
+            "setp.ne.u32 q2, %18, 0;\n\t"
+            "setp.ne.u32 q3, %19, 0;\n\t"
+            "@q0 ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%20], %24;\n\t"
+            "@q1 ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%4, %5, %6, %7}, [%21], %25;\n\t"
+            "@q2 ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%8, %9, %10, %11}, [%22], %26;\n\t"
+            "@q3 ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%12, %13, %14, %15}, [%23], %27;\n\t"
+            "}"
+            : "+r"(v[0].x), "+r"(v[0].y), "+r"(v[0].z), "+r"(v[0].w), "+r"(v[1].x), "+r"(v[1].y), "+r"(v[1].z),
+              "+r"(v[1].w), "+r"(v[2].x), "+r"(v[2].y), "+r"(v[2].z), "+r"(v[2].w), "+r"(v[3].x), "+r"(v[3].y),
+              "+r"(v[3].z), "+r"(v[3].w)
+            : "r"((unsigned)p[0]), "r"((unsigned)p[1]), "r"((unsigned)p[2]), "r"((unsigned)p[3]), "l"(a[0]),
+              "l"(a[1]), "l"(a[2]), "l"(a[3]), "l"(pol[0]), "l"(pol[1]), "l"(pol[2]), "l"(pol[3]));
+    else
+        asm volatile(
+            "{\n\t.reg .pred q0, q1, q2, q3;\n\t"
+            "setp.ne.u32 q0, %16, 0;\n\t"
+            "setp.ne.u32 q1, %17, 0;\n\t"
+            "setp.ne.u32 q2, %18, 0;\n\t"
+            "setp.ne.u32 q3, %19, 0;\n\t"
+            "@q0 ld.global.nc.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%20], %24;\n\t"
+            "@q1 ld.global.nc.L2::cache_hint.v4.u32 {%4, %5, %6, %7}, [%21], %25;\n\t"
+            "@q2 ld.global.nc.L2::cache_hint.v4.u32 {%8, %9, %10, %11}, [%22], %26;\n\t"
+            "@q3 ld.global.nc.L2::cache_hint.v4.u32 {%12, %13, %14, %15}, [%23], %27;\n\t"
+            "}"
+            : "+r"(v[0].x), "+r"(v[0].y), "+r"(v[0].z), "+r"(v[0].w), "+r"(v[1].x), "+r"(v[1].y), "+r"(v[1].z),
+              "+r"(v[1].w), "+r"(v[2].x), "+r"(v[2].y), "+r"(v[2].z), "+r"(v[2].w), "+r"(v[3].x), "+r"(v[3].y),
+              "+r"(v[3].z), "+r"(v[3].w)
+            : "r"((unsigned)p[0]), "r"((unsigned)p[1]), "r"((unsigned)p[2]), "r"((unsigned)p[3]), "l"(a[0]),
+              "l"(a[1]), "l"(a[2]), "l"(a[3]), "l"(pol[0]), "l"(pol[1]), "l"(pol[2]), "l"(pol[3]));
+}
+template <bool NA>
+__device__ __forceinline__ void ldgq_pol(const uint4* const (&a)[2], const bool (&p)[2], const uint64_t (&pol)[2],
+                                         uint4 (&v)[2]) {
+    asm volatile(
+        "{\n\t.reg .pred q0, q1;\n\t"
+        "setp.ne.u32 q0, %8, 0;\n\t"
+        "setp.ne.u32 q1, %9, 0;\n\t"
+        "@q0 ld.global.nc.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%10], %12;\n\t"
+        "@q1 ld.global.nc.L2::cache_hint.v4.u32 {%4, %5, %6, %7}, [%11], %13;\n\t"
+        "}"
+        : "+r"(v[0].x), "+r"(v[0].y), "+r"(v[0].z), "+r"(v[0].w), "+r"(v[1].x), "+r"(v[1].y), "+r"(v[1].z),
+          "+r"(v[1].w)
+        : "r"((unsigned)p[0]), "r"((unsigned)p[1]), "l"(a[0]), "l"(a[1]), "l"(pol[0]), "l"(pol[1]));
+}
+
 template <bool NA>
 __device__ __forceinline__ void ldgq(const uint4* const (&a)[4], const bool (&p)[4], uint4 (&v)[4]) {
     if constexpr (NA) ldg4q_na(a, p, v);
@@ -151,5 +218,44 @@ __device__ __forceinline__ void ldgq(const uint4* const (&a)[4], const bool (&p)
 }
 template <bool NA>
 __device__ __forceinline__ void ldgq(const uint4* const (&a)[2], const bool (&p)[2], uint4 (&v)[2]) { ldg2q(a, p, v); }
+
+// ---- mbarrier + bulk asynchronous copies (TMA engine, SASS UBLKCP) ----------
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+// make barrier inits visible to the async proxy (the bulk copies' complete_tx)
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+// order this thread's earlier generic-proxy shared accesses before later
+// async-proxy (bulk copy) writes to the same buffer
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+// global -> shared bulk copy of `bytes` (multiple of 16, 16-byte aligned both
+// sides) completing `bytes` of transaction count on `bar`
+__device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_pol(unsigned dst, const void* src, unsigned bytes, unsigned bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(unsigned bar, unsigned parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+    while (!mbar_try_wait(bar, parity)) {
+    }
+}
 
 }  // namespace trigpu

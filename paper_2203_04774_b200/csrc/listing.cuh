@@ -55,6 +55,8 @@ struct ListParams {
     unsigned int* queue;      // dynamic work counter
     uint32_t* bitmaps;        // class G only: one n-bit bitmap per CTA
     uint64_t bitmap_words;
+    uint32_t hot_rank;        // rows of ranks >= hot_rank (the most re-read ones) are loaded evict_last
+    uint32_t hist_base;       // per-vertex counts of ranks >= hist_base are kept per CTA in shared memory
     int variant;              // TL_DEBUG_VARIANT: 2 = null probe (experiments build, timing only)
     uint32_t bm_shrink;       // TL_DEBUG_BM_SHRINK: smaller windows (tests force the below-window path)
 };
@@ -171,21 +173,6 @@ struct RowVerify {  // branch-free binary search of the seed's sorted set row (L
     }
 };
 
-// Class G: exact n-bit bitmap in global memory (L2-resident per CTA).
-struct BitmapProbe {
-    static constexpr bool low = false;
-    const uint32_t* bm;
-    uint32_t n;  // bits n .. are the always-zero slack words
-    __device__ __forceinline__ uint32_t bit(uint32_t y) const {
-        y = min(y, n);  // pad slots (kNone) read the zero slack
-        return (__ldcg(bm + (y >> 5)) >> (y & 31)) & 1u;
-    }
-    __device__ __forceinline__ bool below(uint32_t) const { return false; }
-    __device__ __forceinline__ uint32_t cand(uint32_t) const { return 0u; }
-    __device__ __forceinline__ bool verify(uint32_t, bool act) const { return act; }
-    __device__ __forceinline__ uint32_t sentinel() const { return n; }
-};
-
 // Timing-only probe (TL_DEBUG_VARIANT 2 in a -DTRIGPU_EXPERIMENTS build):
 // touches every loaded element, never hits. Measures the row-streaming limit.
 struct NullProbe {
@@ -214,26 +201,48 @@ __device__ __forceinline__ bool probe_one(const Probe& probe, uint32_t y, bool a
 // (s, x, y) of h(s) h(x) h(y) (common.cuh), h from the per-rank table hv; with
 // the count + checksum sinks nothing is buffered: a chunk's hits add their
 // h(y) lane-locally and one multiply by h(s) h(x) folds them in (kFastSum).
-// Per-vertex counts and lists go through the warp's hit buffer (emit).
+// Lists go through the warp's hit buffer (emit). Per-vertex counts are added
+// where the hits are found: one atomic per chunk for its row owner x (all of
+// a chunk's hits share x), one per hit for y, and one per seed; counts of the
+// top kHist ranks (the hubs, which most hits land on under degree order) go
+// to a per-CTA shared-memory histogram flushed once at the end of the kernel,
+// the rest to global memory.
+constexpr uint32_t kHist = 4096;
 template <int ALGO, unsigned F>
 struct Sink {
-    static constexpr bool kFastSum = (F & F_CHECKSUM) != 0u && (F & (F_VCOUNT | F_LIST)) == 0u;
-    static constexpr bool kBuffered = (F & (F_VCOUNT | F_LIST)) != 0u;
+    static constexpr bool kFastSum = (F & F_CHECKSUM) != 0u && (F & F_LIST) == 0u;
+    static constexpr bool kBuffered = (F & F_LIST) != 0u;
     unsigned long long cnt = 0, sum = 0;
     unsigned long long hs = 0;    // h(seed)
     unsigned long long acc = 0;   // this seed's sum of h(x) h(y); times h(s) at end_unit
     unsigned seed_hits = 0;
     unsigned buf = 0;      // shared address of this warp's kHitBuf uint2 entries
     unsigned pending = 0;  // warp-uniform
+    uint32_t* hist = nullptr;  // the CTA's kHist counters (F_VCOUNT)
+
+    // c more triangles containing vertex v (rank)
+    __device__ __forceinline__ void vc_add(const ListParams& P, uint32_t v, unsigned c) {
+        if constexpr ((F & F_VCOUNT) != 0u) {
+            if (v >= P.hist_base) atomicAdd(hist + (v - P.hist_base), c);
+            else atomicAdd(&P.vcount[v], (unsigned long long)c);
+        }
+    }
 
     __device__ __forceinline__ void begin_unit(const ListParams& P, uint32_t seed) {
         if constexpr ((F & F_CHECKSUM) != 0u) hs = __ldg(P.hv + seed);
     }
 
-    // One hit with its own x (short-row stream), kFastSum only.
+    // One hit with its own x (short-row stream).
     __device__ __forceinline__ void direct(const ListParams& P, bool hit, uint32_t x, uint32_t y) {
         if constexpr (kFastSum)
             if (hit) acc += __ldg(P.hv + x) * __ldg(P.hv + y);
+        if constexpr ((F & F_VCOUNT) != 0u) {
+            if (hit) {
+                vc_add(P, x, 1);
+                vc_add(P, y, 1);
+            }
+            seed_hits += hit;
+        }
     }
 
     // One 32-wide batch of hits (called convergently by the warp), kBuffered only.
@@ -252,15 +261,6 @@ struct Sink {
         const bool hit = lane < n;
         const uint2 e = hit ? lds64(from + 8u * lane) : make_uint2(0, 0);
         const uint32_t x = e.x, y = e.y;
-        if constexpr ((F & F_VCOUNT) != 0u) {
-            // hubs recur within the 32 entries (same x for a chunk's hits,
-            // the same hub y for many x): one atomic per distinct vertex
-            const unsigned gx = __match_any_sync(FULL, hit ? x : kNone);
-            const unsigned gy = __match_any_sync(FULL, hit ? y : kNone);
-            if (hit && (gx & lanemask_lt()) == 0) atomicAdd(&P.vcount[x], (unsigned long long)__popc(gx));
-            if (hit && (gy & lanemask_lt()) == 0) atomicAdd(&P.vcount[y], (unsigned long long)__popc(gy));
-            seed_hits += hit;
-        }
         if constexpr ((F & F_CHECKSUM) != 0u)
             if (hit) acc += __ldg(P.hv + x) * __ldg(P.hv + y);
         if constexpr ((F & F_LIST) != 0u) {
@@ -336,7 +336,14 @@ struct Sink {
 // are predicated off and their bits masked. The chunks come from a Cursor
 // (rows held by the lanes, or a CTA's shared row table), four at a time; one
 // batch may span several rows.
+#ifndef TRIGPU_L2HINT
+#define TRIGPU_L2HINT 0
+#endif
+#ifndef TRIGPU_CKS
+#define TRIGPU_CKS 0
+#endif
 constexpr uint32_t kLongRow = 96;  // rows at least this long are read in quad chunks
+constexpr uint32_t kSlotBytes = 512;  // one chunk (32 quads) in a shared-memory stage
 constexpr int kQU = 4;             // chunks per batch
 
 struct Chunk {
@@ -347,6 +354,144 @@ struct Chunk {
 
 // chunks of a row of nqr quads
 __device__ __forceinline__ uint32_t row_chunks(uint32_t nqr) { return (nqr + 31u) >> 5; }
+
+// Probe QU quads (one per chunk, lane l holding quad l of each) against the
+// seed's set and feed the hits to the sink. pr[i]: the lane's quad i is part
+// of chunk i; ch[i].x owns chunk i.
+template <int QU, int ALGO, unsigned F, class Probe, bool kStaged = false>
+__device__ __forceinline__ void probe_quads(const ListParams& P, uint32_t seed, const Chunk (&ch)[QU], const bool (&pr)[QU],
+                                            const uint4 (&y)[QU], const Probe& probe, Sink<ALGO, F>& sink,
+                                            unsigned& hits, unsigned stage = 0) {
+    uint32_t hb[QU];
+    bool any = false;
+#pragma unroll
+    for (int i = 0; i < QU; ++i) {
+        hb[i] = probe.bit(y[i].x) | (probe.bit(y[i].y) << 1) | (probe.bit(y[i].z) << 2) | (probe.bit(y[i].w) << 3);
+        hb[i] = pr[i] ? hb[i] : 0u;
+        // a quad's first element is its smallest (rows sorted, pads last)
+        if constexpr (Probe::low) any |= pr[i] && probe.below(y[i].x);
+    }
+    if constexpr (Probe::low) {
+        // elements below the window: region-B candidates, verified here
+        if (__any_sync(FULL, any)) {
+#pragma unroll
+            for (int i = 0; i < QU; ++i) {
+                if (!__any_sync(FULL, pr[i] && probe.below(y[i].x))) continue;
+                const uint32_t e[4] = {y[i].x, y[i].y, y[i].z, y[i].w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const bool c = pr[i] && probe.below(e[k]) && probe.cand(e[k]);
+                    if (__any_sync(FULL, c))
+                        if (probe.verify(e[k], c)) hb[i] |= 1u << k;
+                }
+            }
+        }
+    }
+    uint32_t hm = 0;
+#pragma unroll
+    for (int i = 0; i < QU; ++i) hm |= hb[i] << (4 * i);
+    hits += __popc(hm);
+    if constexpr ((F & F_VCOUNT) != 0u) {
+        sink.seed_hits += __popc(hm);
+        if (__any_sync(FULL, hm != 0)) {
+#pragma unroll
+            for (int i = 0; i < QU; ++i) {  // x side: one atomic per chunk
+                const unsigned c = __reduce_add_sync(FULL, __popc(hb[i]));
+                if (lane_id() == 0 && c) sink.vc_add(P, ch[i].x, c);
+            }
+#pragma unroll
+            for (int i = 0; i < QU; ++i) {  // y side: per hit
+                if (hb[i] & 1u) sink.vc_add(P, y[i].x, 1);
+                if (hb[i] & 2u) sink.vc_add(P, y[i].y, 1);
+                if (hb[i] & 4u) sink.vc_add(P, y[i].z, 1);
+                if (hb[i] & 8u) sink.vc_add(P, y[i].w, 1);
+            }
+        }
+    }
+    if constexpr (Sink<ALGO, F>::kBuffered) {
+        if (__any_sync(FULL, hm != 0)) {
+#pragma unroll
+            for (int i = 0; i < QU; ++i) {
+                if (__any_sync(FULL, hb[i] != 0)) {
+                    sink.batch(hb[i] & 1u, ch[i].x, y[i].x);
+                    sink.batch(hb[i] & 2u, ch[i].x, y[i].y);
+                    sink.drain(P, seed);
+                    sink.batch(hb[i] & 4u, ch[i].x, y[i].z);
+                    sink.batch(hb[i] & 8u, ch[i].x, y[i].w);
+                    sink.drain(P, seed);
+                }
+            }
+        }
+    } else if constexpr (Sink<ALGO, F>::kFastSum && kStaged) {
+        // the chunks sit in shared memory (the stage): walk each lane's hit
+        // bits, reading the hit element back from the stage, so only hits
+        // cost gathers (a warp iterates max over lanes of its hit count,
+        // ~3, instead of once per element slot)
+        if (__any_sync(FULL, hm != 0)) {
+            const unsigned long long* hv;
+            asm("mov.b64 %0, %1;" : "=l"(hv) : "l"(P.hv));
+            unsigned long long hx[QU];
+#pragma unroll
+            for (int i = 0; i < QU; ++i) hx[i] = __ldg(hv + ch[i].x);
+            unsigned long long a = 0;
+            uint32_t b = hm;
+            const unsigned lane16 = stage + 16u * lane_id();
+            while (__any_sync(FULL, b != 0)) {
+                if (b) {
+                    const uint32_t bit = __ffs(b) - 1;
+                    b &= b - 1;
+                    const uint32_t i = bit >> 2;
+                    const uint32_t yv = lds32(lane16 + i * kSlotBytes + 4u * (bit & 3u));
+                    unsigned long long h = hx[0];
+#pragma unroll
+                    for (int j = 1; j < QU; ++j) h = i == (uint32_t)j ? hx[j] : h;
+                    a += h * __ldg(hv + yv);
+                }
+            }
+            sink.acc += a;
+        }
+    } else if constexpr (Sink<ALGO, F>::kFastSum) {
+        // per chunk: sum over its hits y of h(y), then one multiply by
+        // h(s) h(x). Straight-line gathers (hub ranks: L1/L2 hits), all in
+        // flight before the first use.
+        if (__any_sync(FULL, hm != 0)) {
+            // hv base held in a register (else it is re-read from the
+            // constant bank per predicated load)
+            const unsigned long long* hv;
+            asm("mov.b64 %0, %1;" : "=l"(hv) : "l"(P.hv));
+            unsigned long long sy[QU];
+#if TRIGPU_CKS == 1
+            // conditional loads: only hit lanes generate memory requests
+#pragma unroll
+            for (int i = 0; i < QU; ++i) {
+                unsigned long long a = 0;
+                if (hb[i] & 1u) a += __ldg(hv + y[i].x);
+                if (hb[i] & 2u) a += __ldg(hv + y[i].y);
+                if (hb[i] & 4u) a += __ldg(hv + y[i].z);
+                if (hb[i] & 8u) a += __ldg(hv + y[i].w);
+                sy[i] = a;
+            }
+#pragma unroll
+            for (int i = 0; i < QU; ++i)
+                if (hb[i]) sink.acc += sy[i] * __ldg(hv + ch[i].x);
+#else
+            // lanes without a hit read hv[n] = 0, so the loads need no predicate
+            const uint32_t zero = P.n;
+#pragma unroll
+            for (int i = 0; i < QU; ++i) {
+                const unsigned long long a0 = __ldg(hv + ((hb[i] & 1u) ? y[i].x : zero));
+                const unsigned long long a1 = __ldg(hv + ((hb[i] & 2u) ? y[i].y : zero));
+                const unsigned long long a2 = __ldg(hv + ((hb[i] & 4u) ? y[i].z : zero));
+                const unsigned long long a3 = __ldg(hv + ((hb[i] & 8u) ? y[i].w : zero));
+                sy[i] = (a0 + a1) + (a2 + a3);
+            }
+#pragma unroll
+            for (int i = 0; i < QU; ++i)
+                if (hb[i]) sink.acc += sy[i] * __ldg(hv + ch[i].x);
+#endif
+        }
+    }
+}
 
 template <int ALGO, unsigned F, bool kSparse, class Probe, class Cursor>
 __device__ __forceinline__ void stream_quads(const ListParams& P, uint32_t seed, Cursor& cur, const Probe& probe,
@@ -359,6 +504,9 @@ __device__ __forceinline__ void stream_quads(const ListParams& P, uint32_t seed,
     uint4 y[QU];
 #pragma unroll
     for (int i = 0; i < QU; ++i) y[i] = make_uint4(kNone, kNone, kNone, kNone);
+#if TRIGPU_L2HINT
+    const uint64_t pol_last = l2_policy_last(), pol_first = l2_policy_first();
+#endif
     while (cur.more()) {
         Chunk ch[QU];
         cur.next(ch);
@@ -369,75 +517,15 @@ __device__ __forceinline__ void stream_quads(const ListParams& P, uint32_t seed,
             pr[i] = lane < ch[i].nq;
             a[i] = quads + (ch[i].qb + lane);
         }
+#if TRIGPU_L2HINT
+        uint64_t pol[QU];
+#pragma unroll
+        for (int i = 0; i < QU; ++i) pol[i] = ch[i].x >= P.hot_rank ? pol_last : pol_first;
+        ldgq_pol<!kSparse>(a, pr, pol, y);
+#else
         ldgq<!kSparse>(a, pr, y);
-        uint32_t hb[QU];
-        bool any = false;
-#pragma unroll
-        for (int i = 0; i < QU; ++i) {
-            hb[i] = probe.bit(y[i].x) | (probe.bit(y[i].y) << 1) | (probe.bit(y[i].z) << 2) | (probe.bit(y[i].w) << 3);
-            hb[i] = pr[i] ? hb[i] : 0u;
-            // a quad's first element is its smallest (rows sorted, pads last)
-            if constexpr (Probe::low) any |= pr[i] && probe.below(y[i].x);
-        }
-        if constexpr (Probe::low) {
-            // elements below the window: region-B candidates, verified here
-            if (__any_sync(FULL, any)) {
-#pragma unroll
-                for (int i = 0; i < QU; ++i) {
-                    if (!__any_sync(FULL, pr[i] && probe.below(y[i].x))) continue;
-                    const uint32_t e[4] = {y[i].x, y[i].y, y[i].z, y[i].w};
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const bool c = pr[i] && probe.below(e[k]) && probe.cand(e[k]);
-                        if (__any_sync(FULL, c))
-                            if (probe.verify(e[k], c)) hb[i] |= 1u << k;
-                    }
-                }
-            }
-        }
-        uint32_t hm = 0;
-#pragma unroll
-        for (int i = 0; i < QU; ++i) hm |= hb[i] << (4 * i);
-        hits += __popc(hm);
-        if constexpr (Sink<ALGO, F>::kBuffered) {
-            if (__any_sync(FULL, hm != 0)) {
-#pragma unroll
-                for (int i = 0; i < QU; ++i) {
-                    if (__any_sync(FULL, hb[i] != 0)) {
-                        sink.batch(hb[i] & 1u, ch[i].x, y[i].x);
-                        sink.batch(hb[i] & 2u, ch[i].x, y[i].y);
-                        sink.drain(P, seed);
-                        sink.batch(hb[i] & 4u, ch[i].x, y[i].z);
-                        sink.batch(hb[i] & 8u, ch[i].x, y[i].w);
-                        sink.drain(P, seed);
-                    }
-                }
-            }
-        } else if constexpr (Sink<ALGO, F>::kFastSum) {
-            // per chunk: sum over its hits y of h(y), then one multiply by
-            // h(s) h(x). Straight-line predicated gathers (hub ranks: L1/L2
-            // hits), all in flight before the first use.
-            if (__any_sync(FULL, hm != 0)) {
-                // hv base held in a register (else it is re-read from the
-                // constant bank per predicated load); lanes without a hit
-                // read hv[n] = 0, so the loads need no predicate
-                const unsigned long long* hv;
-                asm("mov.b64 %0, %1;" : "=l"(hv) : "l"(P.hv));
-                const uint32_t zero = P.n;
-                unsigned long long sy[QU];
-#pragma unroll
-                for (int i = 0; i < QU; ++i) {
-                    const unsigned long long a0 = __ldg(hv + ((hb[i] & 1u) ? y[i].x : zero));
-                    const unsigned long long a1 = __ldg(hv + ((hb[i] & 2u) ? y[i].y : zero));
-                    const unsigned long long a2 = __ldg(hv + ((hb[i] & 4u) ? y[i].z : zero));
-                    const unsigned long long a3 = __ldg(hv + ((hb[i] & 8u) ? y[i].w : zero));
-                    sy[i] = (a0 + a1) + (a2 + a3);
-                }
-#pragma unroll
-                for (int i = 0; i < QU; ++i)
-                    if (hb[i]) sink.acc += sy[i] * __ldg(hv + ch[i].x);
-            }
-        }
+#endif
+        probe_quads<QU>(P, seed, ch, pr, y, probe, sink, hits);
     }
 }
 
@@ -602,15 +690,14 @@ __device__ __forceinline__ void scan_rows(const ListParams& P, uint32_t seed, ui
         const bool hitA = probe_one(probe, yA, actA);
         const bool hitB = probe_one(probe, yB, actB);
         hits += (unsigned)hitA + (unsigned)hitB;
-        if constexpr (Sink<ALGO, F>::kBuffered || Sink<ALGO, F>::kFastSum) {
+        if constexpr (F != 0u) {
             const uint32_t xA = __shfl_sync(FULL, cx, jA), xB = __shfl_sync(FULL, cx, jB);
+            sink.direct(P, hitA, xA, yA);
+            sink.direct(P, hitB, xB, yB);
             if constexpr (Sink<ALGO, F>::kBuffered) {
                 sink.batch(hitA, xA, yA);
                 sink.batch(hitB, xB, yB);
                 sink.drain(P, seed);
-            } else {
-                sink.direct(P, hitA, xA, yA);
-                sink.direct(P, hitB, xB, yB);
             }
         }
     }
@@ -647,13 +734,37 @@ __device__ __forceinline__ void with_win_probe(const ListParams& P, unsigned bma
 // [warps x kHitBuf uint2 hit buffers (buffered sinks only)] followed by the
 // kernel's bitmaps.
 template <unsigned F>
+__host__ __device__ constexpr size_t hitbuf_bytes(int warps) {
+    return (F & F_LIST) ? static_cast<size_t>(warps) * kHitBuf * 8 : 0;
+}
+template <unsigned F>
 __host__ __device__ constexpr size_t warp_scratch_bytes(int warps) {
-    return (F & (F_VCOUNT | F_LIST)) ? static_cast<size_t>(warps) * kHitBuf * 8 : 0;
+    return hitbuf_bytes<F>(warps) + ((F & F_VCOUNT) ? kHist * 4 : 0);
 }
 
+// Point the sink at its scratch and zero the CTA's count histogram (a CTA
+// barrier: call before the work loop, from every thread).
 template <int ALGO, unsigned F>
 __device__ __forceinline__ void attach_scratch(Sink<ALGO, F>& sink, unsigned char* base) {
     sink.buf = smem_addr(base + (threadIdx.x >> 5) * kHitBuf * 8);
+    if constexpr ((F & F_VCOUNT) != 0u) {
+        sink.hist = reinterpret_cast<uint32_t*>(base + hitbuf_bytes<F>(blockDim.x >> 5));
+        for (uint32_t i = threadIdx.x; i < kHist; i += blockDim.x) sink.hist[i] = 0u;
+        __syncthreads();
+    }
+}
+
+// After the work loop, from every thread: add the CTA's histogram to the
+// global per-vertex counts.
+template <int ALGO, unsigned F>
+__device__ __forceinline__ void flush_hist(const ListParams& P, const Sink<ALGO, F>& sink) {
+    if constexpr ((F & F_VCOUNT) != 0u) {
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < kHist; i += blockDim.x) {
+            const uint32_t c = sink.hist[i];
+            if (c) atomicAdd(&P.vcount[P.hist_base + i], (unsigned long long)c);
+        }
+    }
 }
 
 // CTAs per SM of the warp-class kernels: 4 (64 registers) for count only; the
@@ -665,6 +776,25 @@ __device__ __forceinline__ void attach_scratch(Sink<ALGO, F>& sink, unsigned cha
 #define TRIGPU_WARP_MINB_SINK 3
 #endif
 #define WARP_MINB(F) ((F) == 0u ? TRIGPU_WARP_MINB : TRIGPU_WARP_MINB_SINK)
+
+// Seeds handed to a warp in runs of G queue slots per atomic (one atomic per
+// seed on a single counter serialises at its L2 slice when seeds are tiny).
+template <unsigned G>
+struct WarpSeedQueue {
+    unsigned next = 0, end = 0;
+    __device__ __forceinline__ bool pop(const ListParams& P, unsigned& i) {
+        if (next == end) {
+            unsigned b = 0;
+            if (lane_id() == 0) b = atomicAdd(P.queue, G);
+            b = __shfl_sync(FULL, b, 0);
+            if (b >= P.nseeds) return false;
+            next = b;
+            end = min(b + G, P.nseeds);
+        }
+        i = next++;
+        return true;
+    }
+};
 
 // ---- class R: |S| <= 32, warp per seed --------------------------------------
 constexpr int kRWarps = 8;
@@ -684,11 +814,8 @@ __global__ void __launch_bounds__(kRWarps * 32, TRIGPU_WARP_MINB) k_list_reg(Lis
     __syncwarp();
     Sink<ALGO, F> sink;
     attach_scratch(sink, dsm);
-    for (;;) {
-        unsigned i = 0;
-        if (lane == 0) i = atomicAdd(P.queue, 1u);
-        i = __shfl_sync(FULL, i, 0);
-        if (i >= P.nseeds) break;
+    WarpSeedQueue<16> q;
+    for (unsigned i; q.pop(P, i);) {
         const uint32_t seed = P.seeds[i];
         sink.begin_unit(P, seed);
         const uint64_t so = P.set_off[seed];
@@ -706,6 +833,7 @@ __global__ void __launch_bounds__(kRWarps * 32, TRIGPU_WARP_MINB) k_list_reg(Lis
         __syncwarp();
     }
     sink.flush(P);
+    flush_hist(P, sink);
 }
 
 // ---- class H: 32 < |S| <= 256, warp per seed --------------------------------
@@ -748,6 +876,7 @@ __global__ void __launch_bounds__(kHWarps * 32, WARP_MINB(F)) k_list_warp(ListPa
         __syncwarp();
     }
     sink.flush(P);
+    flush_hist(P, sink);
 }
 
 // ---- class C: 256 < |S| <= 4096, CTA per seed ----------------------------------
@@ -757,7 +886,7 @@ __global__ void __launch_bounds__(kHWarps * 32, WARP_MINB(F)) k_list_warp(ListPa
 // balanced work. Two sizes: C1 (256 < |S| <= 1024) runs 8-warp CTAs, several
 // per SM, so one CTA's seed barrier is hidden by the others; C2 (1024 < |S| <=
 // 4096) runs one 32-warp CTA per SM.
-template <int THREADS, uint32_t BITS_A, uint32_t BITS_B, uint32_t MAXD, int MINB>
+template <int THREADS, uint32_t BITS_A, uint32_t BITS_B, uint32_t MAXD, int MINB, int RING = 0>
 struct CtaCfg {
     static constexpr int kThreads = THREADS;
     static constexpr int kWarps = THREADS / 32;
@@ -765,13 +894,104 @@ struct CtaCfg {
     static constexpr uint32_t kBitsB = BITS_B;  // region B of 2^BITS_B bits
     static constexpr uint32_t kMaxD = MAXD;
     static constexpr int kMinBlocks = MINB;
+    static constexpr int kRing = RING;  // 0: register loads; >0: per-warp ring of bulk-copied chunks
 };
-using CfgC1 = CtaCfg<256, 18, 14, 1024, 3>;  // (2^17 window at 4 CTAs/SM: C4 -1 %, C5 +4 %)
-using CfgC2 = CtaCfg<1024, 19, 15, 4096, 1>;  // (2 x 512-thread CTAs, 2^18 window: C5 5 % slower)
+#ifndef TRIGPU_C1_RING
+#define TRIGPU_C1_RING 0
+#endif
+#ifndef TRIGPU_C1_MINB
+#define TRIGPU_C1_MINB 3
+#endif
+#ifndef TRIGPU_C2_RING
+#define TRIGPU_C2_RING 0
+#endif
+#ifndef TRIGPU_C1_BITS_A
+#define TRIGPU_C1_BITS_A 18
+#endif
+#ifndef TRIGPU_H_CTA
+#define TRIGPU_H_CTA 0  // 1: class H as CTA-per-seed staged kernel (CfgH)
+#endif
+#ifndef TRIGPU_H_RING
+#define TRIGPU_H_RING 2
+#endif
+#ifndef TRIGPU_H_MINB
+#define TRIGPU_H_MINB 4
+#endif
+#ifndef TRIGPU_H_BITS_A_CTA
+#define TRIGPU_H_BITS_A_CTA 17
+#endif
+using CfgC1 = CtaCfg<256, TRIGPU_C1_BITS_A, 14, 1024, TRIGPU_C1_MINB, TRIGPU_C1_RING>;  // (2^17 window at 4 CTAs/SM: C4 -1 %, C5 +4 %)
+using CfgC2 = CtaCfg<1024, 19, 15, 4096, 1, TRIGPU_C2_RING>;  // (2 x 512-thread CTAs, 2^18 window: C5 5 % slower)
+using CfgH = CtaCfg<256, TRIGPU_H_BITS_A_CTA, 13, 256, TRIGPU_H_MINB, TRIGPU_H_RING>;
 template <class CFG>
 constexpr size_t cta_bitmap_bytes() { return win_bytes(CFG::kBitsA, CFG::kBitsB); }
 template <class CFG>
 constexpr size_t cta_row_bytes() { return CFG::kMaxD * 16; }  // uint4 {first quad, quads, first chunk, x}
+// per warp: kRing stages of kStageChunks chunks (kSlotBytes each) + per stage
+// an mbarrier (8 B, padded to 16) and kStageChunks {x, quads} records
+constexpr int kStageChunks = 4;
+constexpr uint32_t kStageBytes = kStageChunks * kSlotBytes;
+template <class CFG>
+constexpr size_t cta_ring_bytes() {
+    return static_cast<size_t>(CFG::kWarps) * CFG::kRing * (kStageBytes + 16 + 8 * kStageChunks);
+}
+
+// A warp's contiguous chunk range [gb, ge) of the seed streamed through its
+// ring of NS shared-memory stages of kStageChunks chunks: lane 0 bulk-copies
+// (cp.async.bulk, the TMA engine) the chunks of stage j NS stages ahead of
+// their use and arms the stage's mbarrier with their byte count; every lane
+// waits on it, probes its quads (LDS.128) and, for the checksum, re-reads
+// only its hit elements from the stage. The bytes in flight live in shared
+// memory, not registers. `phases` (bit k = parity to wait for on stage k)
+// persists across seeds.
+template <int NS, int ALGO, unsigned F, class Probe>
+__device__ __forceinline__ void stream_ring(const ListParams& P, uint32_t seed, unsigned rows, uint32_t d,
+                                            uint32_t gb, uint32_t ge, unsigned ring, unsigned bars, unsigned meta,
+                                            uint32_t& phases, const Probe& probe, Sink<ALGO, F>& sink,
+                                            unsigned& hits) {
+    constexpr int K = kStageChunks;
+    const unsigned lane = lane_id();
+    const uint4* const quads = reinterpret_cast<const uint4*>(P.out_adj);
+    CtaRowCursor prod(rows, d, gb, ge);
+    const uint32_t nst = (ge - gb + K - 1) / K;  // stages of this range
+    auto issue = [&](uint32_t k) {
+        Chunk c[K];
+        prod.next(c);
+        if (lane == 0) {
+            unsigned bytes = 0;
+#pragma unroll
+            for (int j = 0; j < K; ++j) bytes += c[j].nq * 16u;
+            sts128(meta + 8u * K * k, make_uint4(c[0].x, c[0].nq, c[1].x, c[1].nq));
+            sts128(meta + 8u * K * k + 16u, make_uint4(c[2].x, c[2].nq, c[3].x, c[3].nq));
+            fence_proxy_async_smem();
+            mbar_arrive_expect_tx(bars + 16u * k, bytes);
+#pragma unroll
+            for (int j = 0; j < K; ++j)
+                if (c[j].nq) bulk_g2s(ring + kStageBytes * k + kSlotBytes * j, quads + c[j].qb, c[j].nq * 16u, bars + 16u * k);
+        }
+    };
+    const uint32_t pro = nst < (uint32_t)NS ? nst : (uint32_t)NS;
+    for (uint32_t k = 0; k < pro; ++k) issue(k);
+    uint32_t k = 0;
+    for (uint32_t i = 0; i < nst; ++i) {
+        mbar_wait(bars + 16u * k, (phases >> k) & 1u);
+        phases ^= 1u << k;
+        const uint4 m0 = lds128(meta + 8u * K * k), m1 = lds128(meta + 8u * K * k + 16u);
+        const Chunk ch[K] = {Chunk{0, m0.y, m0.x}, Chunk{0, m0.w, m0.z}, Chunk{0, m1.y, m1.x}, Chunk{0, m1.w, m1.z}};
+        bool pr[K];
+        uint4 y[K];
+        const unsigned st = ring + kStageBytes * k;
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            pr[j] = lane < ch[j].nq;
+            y[j] = pr[j] ? lds128(st + kSlotBytes * j + 16u * lane) : make_uint4(kNone, kNone, kNone, kNone);
+        }
+        probe_quads<K, ALGO, F, Probe, true>(P, seed, ch, pr, y, probe, sink, hits, st);
+        __syncwarp();
+        if (i + NS < nst) issue(k);
+        k = k + 1 == (uint32_t)NS ? 0 : k + 1;
+    }
+}
 
 template <int ALGO, unsigned F, class CFG>
 __global__ void __launch_bounds__(CFG::kThreads, CFG::kMinBlocks) k_list_cta(ListParams P) {
@@ -785,6 +1005,17 @@ __global__ void __launch_bounds__(CFG::kThreads, CFG::kMinBlocks) k_list_cta(Lis
     uint32_t* bmb = bma + ((1u << CFG::kBitsA) / 32 + 4);
     const unsigned rows = smem_addr(dsm + warp_scratch_bytes<F>(CFG::kWarps) + cta_bitmap_bytes<CFG>());
     for (uint32_t i = threadIdx.x; i < kWords; i += kCThreads) bma[i] = 0u;
+    // bulk-copy ring of this warp (kRing > 0): slots | barriers | {x, quads}
+    const unsigned ring_base = rows + cta_row_bytes<CFG>();
+    const unsigned wslot = ring_base + (threadIdx.x >> 5) * CFG::kRing * kStageBytes;
+    const unsigned wbar = ring_base + CFG::kWarps * CFG::kRing * kStageBytes + (threadIdx.x >> 5) * CFG::kRing * 16u;
+    const unsigned wmeta = ring_base + CFG::kWarps * CFG::kRing * (kStageBytes + 16u) +
+                           (threadIdx.x >> 5) * CFG::kRing * 8u * kStageChunks;
+    uint32_t phases = 0;
+    if constexpr (CFG::kRing > 0) {
+        if (lane_id() < (unsigned)CFG::kRing) mbar_init(wbar + 16u * lane_id(), 1);
+        fence_mbar_init();
+    }
     Sink<ALGO, F> sink;
     attach_scratch(sink, dsm);
     constexpr int PER = CFG::kMaxD / kCThreads;  // set elements per thread
@@ -835,9 +1066,13 @@ __global__ void __launch_bounds__(CFG::kThreads, CFG::kMinBlocks) k_list_cta(Lis
             const uint32_t gb = static_cast<uint32_t>((static_cast<uint64_t>(nchunks) * warp) / CFG::kWarps);
             const uint32_t ge = static_cast<uint32_t>((static_cast<uint64_t>(nchunks) * (warp + 1)) / CFG::kWarps);
             if (gb < ge) {
-                CtaRowCursor cur(rows, d, gb, ge);
                 unsigned hits = 0;
-                stream_quads<ALGO, F, false>(P, seed, cur, probe, sink, hits);
+                if constexpr (CFG::kRing > 0) {
+                    stream_ring<CFG::kRing>(P, seed, rows, d, gb, ge, wslot, wbar, wmeta, phases, probe, sink, hits);
+                } else {
+                    CtaRowCursor cur(rows, d, gb, ge);
+                    stream_quads<ALGO, F, false>(P, seed, cur, probe, sink, hits);
+                }
                 sink.cnt += hits;
             }
         });
@@ -846,11 +1081,38 @@ __global__ void __launch_bounds__(CFG::kThreads, CFG::kMinBlocks) k_list_cta(Lis
         for (uint32_t k = threadIdx.x; k < d; k += kCThreads) win_clear(bma, bmb, g, __ldg(row + k));
     }
     sink.flush(P);
+    flush_hist(P, sink);
 }
 
-// ---- class G: |S| > 4096, CTA per seed, global bitmap --------------------
-constexpr int kGThreads = 512;
+// ---- class G: |S| > 4096, CTA per seed ---------------------------------------
+// A 2^20-rank shared-memory window over the set's top ranks (as the other
+// classes), and for the set's elements below the window an exact n-bit
+// bitmap in global memory (one per CTA, L2-resident slices): elements above
+// the set's top rank cost one LDS of the guard word, elements in the window
+// one LDS, only elements below the window touch the global bitmap (no
+// verification needed: it is exact).
+constexpr int kGThreads = 1024;
 constexpr int kGWarps = kGThreads / 32;
+#ifndef TRIGPU_G_BITS_A
+#define TRIGPU_G_BITS_A 20
+#endif
+constexpr uint32_t kGBitsA = TRIGPU_G_BITS_A;
+constexpr size_t kGWinBytes = (size_t{1} << kGBitsA) / 8 + 16;
+
+struct WinGlobalProbe {
+    static constexpr bool low = true;
+    unsigned bm;          // shared address of the window
+    uint32_t wb, la;      // window base, length
+    const uint32_t* gbm;  // exact global bitmap of the set's elements below wb
+    __device__ __forceinline__ uint32_t bit(uint32_t y) const {
+        const uint32_t o = min(y - wb, la);
+        return (lds32(bm + ((o >> 5) << 2)) >> (o & 31u)) & 1u;
+    }
+    __device__ __forceinline__ bool below(uint32_t y) const { return y < wb; }
+    __device__ __forceinline__ uint32_t cand(uint32_t y) const { return (__ldcg(gbm + (y >> 5)) >> (y & 31u)) & 1u; }
+    __device__ __forceinline__ bool verify(uint32_t, bool act) const { return act; }
+    __device__ __forceinline__ uint32_t sentinel() const { return kNone; }
+};
 
 template <int ALGO, unsigned F>
 __global__ void __launch_bounds__(kGThreads) k_list_giant(ListParams P) {
@@ -858,6 +1120,9 @@ __global__ void __launch_bounds__(kGThreads) k_list_giant(ListParams P) {
     __shared__ unsigned unit;
     const unsigned warp = threadIdx.x >> 5;
     uint32_t* bm = P.bitmaps + (uint64_t)blockIdx.x * P.bitmap_words;
+    uint32_t* win = reinterpret_cast<uint32_t*>(dsm + warp_scratch_bytes<F>(kGWarps));
+    constexpr uint32_t kWords = kGWinBytes / 4;
+    for (uint32_t i = threadIdx.x; i < kWords; i += kGThreads) win[i] = 0u;
     Sink<ALGO, F> sink;
     attach_scratch(sink, dsm);
     for (;;) {
@@ -870,28 +1135,35 @@ __global__ void __launch_bounds__(kGThreads) k_list_giant(ListParams P) {
         sink.begin_unit(P, seed);
         const uint64_t so = P.set_off[seed];
         const uint32_t d = P.set_len[seed];
+        const uint32_t* row = P.set_adj + so;
+        const uint32_t la = 1u << (kGBitsA > P.bm_shrink + 5u ? kGBitsA - P.bm_shrink : 5u);
+        const uint32_t s0 = __ldg(row), top = __ldg(row + d - 1);
+        const uint32_t wb = top - s0 >= la ? top + 1u - la : s0;
         for (uint32_t k = threadIdx.x; k < d; k += kGThreads) {
-            const uint32_t v = __ldg(P.set_adj + so + k);
-            atomicOr(bm + (v >> 5), 1u << (v & 31));
+            const uint32_t v = __ldg(row + k);
+            if (v >= wb) atomicOr(win + ((v - wb) >> 5), 1u << ((v - wb) & 31u));
+            else atomicOr(bm + (v >> 5), 1u << (v & 31));
         }
         __syncthreads();
-        const BitmapProbe probe{bm, P.n};
+        const WinGlobalProbe probe{smem_addr(win), wb, la, bm};
         scan_x_range<ALGO, F>(P, seed, so, warp * 32, d, kGWarps * 32, probe, sink);
         sink.end_unit(P, seed);
         __syncthreads();
         for (uint32_t k = threadIdx.x; k < d; k += kGThreads) {
-            const uint32_t v = __ldg(P.set_adj + so + k);
-            __stcg(bm + (v >> 5), 0u);
+            const uint32_t v = __ldg(row + k);
+            if (v >= wb) win[(v - wb) >> 5] = 0u;
+            else __stcg(bm + (v >> 5), 0u);
         }
     }
     sink.flush(P);
+    flush_hist(P, sink);
 }
 
 // dynamic shared memory per CTA of each class kernel
 template <unsigned F> constexpr size_t smem_reg() { return warp_scratch_bytes<F>(kRWarps) + kRWarps * kRBmBytes; }
 template <unsigned F> constexpr size_t smem_warp() { return warp_scratch_bytes<F>(kHWarps) + kHWarps * kHBmBytes; }
-template <unsigned F, class CFG> constexpr size_t smem_cta() { return warp_scratch_bytes<F>(CFG::kWarps) + cta_bitmap_bytes<CFG>() + cta_row_bytes<CFG>(); }
-template <unsigned F> constexpr size_t smem_giant() { return warp_scratch_bytes<F>(kGWarps); }
+template <unsigned F, class CFG> constexpr size_t smem_cta() { return warp_scratch_bytes<F>(CFG::kWarps) + cta_bitmap_bytes<CFG>() + cta_row_bytes<CFG>() + cta_ring_bytes<CFG>(); }
+template <unsigned F> constexpr size_t smem_giant() { return warp_scratch_bytes<F>(kGWarps) + kGWinBytes; }
 
 // ---- seed classification --------------------------------------------------
 constexpr int kClasses = 5;  // R, H, C1, C2, G
@@ -901,15 +1173,17 @@ struct SeedLists {
     unsigned int* counts;     // [kClasses]
 };
 
-__global__ void __launch_bounds__(256) k_classify_seeds(uint32_t n, const uint32_t* __restrict__ set_len,
+// Seeds with rank in [rb, re) and |S| >= 2 into their class lists.
+__global__ void __launch_bounds__(256) k_classify_seeds(uint32_t rb, uint32_t re, const uint32_t* __restrict__ set_len,
                                                         SeedLists L) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const uint64_t start = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    const uint64_t trips = (n + stride - 1) / stride;
+    const uint64_t span = re - rb;
+    const uint64_t trips = (span + stride - 1) / stride;
     for (uint64_t t = 0; t < trips; ++t) {
-        const uint64_t r = start + t * stride;
+        const uint64_t r = rb + start + t * stride;
         uint64_t d = 0;
-        if (r < n) d = set_len[r];
+        if (r < re) d = set_len[r];
         int cls = -1;
         if (d >= 2) cls = d <= 32 ? 0 : d <= 256 ? 1 : d <= CfgC1::kMaxD ? 2 : d <= CfgC2::kMaxD ? 3 : 4;
 #pragma unroll
@@ -922,6 +1196,31 @@ __global__ void __launch_bounds__(256) k_classify_seeds(uint32_t n, const uint32
             base = __shfl_sync(FULL, base, leader);
             if (cls == c) L.lists[c][base + __popc(b & lanemask_lt())] = (uint32_t)r;
         }
+    }
+}
+
+// inner_ops / mark_ops of the seeds in [rb, re) (tl_list_range): per seed s,
+// inner += sum over x in set(s) of d+(x) (listing.hpp:80, 101), mark += 2|S|.
+// Warp per seed.
+__global__ void __launch_bounds__(256) k_range_cost(uint32_t rb, uint32_t re, const uint64_t* __restrict__ set_off,
+                                                    const uint32_t* __restrict__ set_len,
+                                                    const uint32_t* __restrict__ set_adj,
+                                                    const uint32_t* __restrict__ out_len,
+                                                    unsigned long long* __restrict__ acc) {
+    const unsigned lane = lane_id();
+    const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    unsigned long long inner = 0, mark = 0;
+    for (uint64_t r = rb + ((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5); r < re; r += warps) {
+        const uint64_t so = set_off[r];
+        const uint32_t d = set_len[r];
+        if (lane == 0) mark += 2ull * d;
+        for (uint32_t i = lane; i < d; i += 32) inner += out_len[set_adj[so + i]];
+    }
+    inner = warp_sum64(inner);
+    mark = warp_sum64(mark);
+    if (lane == 0) {
+        atomicAdd(&acc[0], inner);
+        atomicAdd(&acc[1], mark);
     }
 }
 

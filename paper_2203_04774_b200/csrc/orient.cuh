@@ -482,6 +482,21 @@ __global__ void k_pad_len(uint32_t n, const uint32_t* __restrict__ deg, uint32_t
         plen[r] = (deg[r] + 3u) & ~3u;
 }
 
+// Lowest rank r whose out-rows [r, n) fit in `budget_elems` padded elements:
+// the rows the listing loads with L2 evict_last (the top ranks are the rows
+// re-read by the most seeds). One thread, binary search over out_off.
+__global__ void k_hot_rank(uint32_t n, const uint64_t* __restrict__ out_off, uint64_t budget_elems,
+                           unsigned long long* __restrict__ out) {
+    const uint64_t end = out_off[n];
+    uint32_t lo = 0, hi = n;  // find min r with end - out_off[r] <= budget
+    while (lo < hi) {
+        const uint32_t mid = lo + (hi - lo) / 2;
+        if (end - out_off[mid] <= budget_elems) hi = mid;
+        else lo = mid + 1;
+    }
+    *out = lo;
+}
+
 // Checksum sink table: hv[r] = vertex_hash(inv[r]) (common.cuh).
 __global__ void k_vertex_hash(uint32_t n, const uint32_t* __restrict__ inv, unsigned long long* __restrict__ hv) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;

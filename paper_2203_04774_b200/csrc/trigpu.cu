@@ -39,6 +39,13 @@ namespace {
 
 thread_local std::string g_create_error;
 
+#ifndef TRIGPU_HOT_MB
+#define TRIGPU_HOT_MB 64
+#endif
+// L2 budget for the evict_last rows (126 MB L2: leave room for the checksum
+// table gathers and the cold streaming)
+constexpr uint64_t kHotRowBytes = uint64_t{TRIGPU_HOT_MB} << 20;
+
 enum Phase {
     PH_H2D = 0,
     PH_RELABEL,
@@ -88,6 +95,7 @@ struct tl_ctx {
     uint32_t norm_n = 0;
     uint64_t norm_m = 0;
     uint32_t max_out = 0;
+    uint32_t hot_rank = 0;  // rows of ranks >= hot_rank fit the L2 evict_last budget
     unsigned long long cost[4] = {0, 0, 0, 0};
     double h2d_ms = 0, orient_ms = 0;
 
@@ -314,6 +322,8 @@ tl_status orient_core(tl_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* goff,
         k_maxdeg<<<grid_for(n, 256, ctx->sms * 4), 256, 0, ctx->s>>>(n, P<uint32_t>(ctx->outdeg),
                                                                     reinterpret_cast<unsigned int*>(flags + 6));
         LAUNCHED();
+        k_hot_rank<<<1, 1, 0, ctx->s>>>(n, P<uint64_t>(ctx->out_off), kHotRowBytes / 4, flags + 10);
+        LAUNCHED();
     }
     CK(cudaEventRecord(ctx->ev[PH_COST], ctx->s));
     unsigned long long res[6];
@@ -323,6 +333,12 @@ tl_status orient_core(tl_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* goff,
         return ctx->fail(TL_ERR_INVALID_ARGUMENT, "orient: adjacency is not symmetric (out-degrees do not sum to m)");
     std::memcpy(ctx->cost, res, sizeof(ctx->cost));
     ctx->max_out = static_cast<uint32_t>(res[4]);
+    unsigned long long hot = n;
+    if (n) {
+        CK(cudaMemcpyAsync(&hot, flags + 10, 8, cudaMemcpyDeviceToHost, ctx->s));
+        CK(cudaStreamSynchronize(ctx->s));
+    }
+    ctx->hot_rank = static_cast<uint32_t>(hot);
     ctx->phase_ms[PH_RELABEL] = ev_ms(ctx->ev[PH_H2D], ctx->ev[PH_RELABEL]);
     ctx->phase_ms[PH_SCAN] = ev_ms(ctx->ev[PH_RELABEL], ctx->ev[PH_SCAN]);
     ctx->phase_ms[PH_SCATTER] = ev_ms(ctx->ev[PH_SCAN], ctx->ev[PH_SCATTER]);
@@ -469,6 +485,12 @@ tl_status launch_classes(tl_ctx* ctx, ListParams base, uint32_t* const lists[kCl
         ctx->cls_run[0] = true;
     }
     if (h[1]) {
+#if TRIGPU_H_CTA
+        CK(cudaEventRecord(ctx->cls_ev[2], ctx->s));
+        st = launch_cta<ALGO, F, CfgH>(ctx, base, lists[1], h[1], queues + 1);
+        if (st != TL_OK) return st;
+        CK(cudaEventRecord(ctx->cls_ev[3], ctx->s));
+#else
         ListParams p = base;
         p.seeds = lists[1];
         p.nseeds = h[1];
@@ -481,6 +503,7 @@ tl_status launch_classes(tl_ctx* ctx, ListParams base, uint32_t* const lists[kCl
         k_list_warp<ALGO, F><<<grid, kHWarps * 32, smem, ctx->s>>>(p);
         LAUNCHED();
         CK(cudaEventRecord(ctx->cls_ev[3], ctx->s));
+#endif
         ctx->cls_run[1] = true;
     }
     if (h[2]) {
@@ -874,6 +897,12 @@ TL_API tl_status tl_orient_device(tl_ctx* ctx, uint32_t n, uint64_t m, const uin
 
 TL_API tl_status tl_list(tl_ctx* ctx, int algo, unsigned out_flags, tl_stats* out) {
     if (!ctx) return TL_ERR_INVALID_ARGUMENT;
+    return tl_list_range(ctx, algo, out_flags, 0, ctx->n, out);
+}
+
+TL_API tl_status tl_list_range(tl_ctx* ctx, int algo, unsigned out_flags, uint32_t rank_begin, uint32_t rank_end,
+                               tl_stats* out) {
+    if (!ctx) return TL_ERR_INVALID_ARGUMENT;
     if (!ctx->oriented) return ctx->fail(TL_ERR_STATE, "tl_list: no oriented view (call tl_orient first)");
     if (algo != TL_ALGO_APP && algo != TL_ALGO_APM) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "tl_list: algo must be TL_ALGO_APP or TL_ALGO_APM");
     if (out_flags & ~7u) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "tl_list: unknown output flag");
@@ -881,6 +910,9 @@ TL_API tl_status tl_list(tl_ctx* ctx, int algo, unsigned out_flags, tl_stats* ou
     if ((uint64_t)ctx->max_out * 32 >= (1ull << 32))
         return ctx->fail(TL_ERR_INVALID_ARGUMENT, "tl_list: out-degree >= 2^27 is not supported");
     const uint32_t n = ctx->n;
+    if (rank_begin > rank_end || rank_end > n)
+        return ctx->fail(TL_ERR_INVALID_ARGUMENT, "tl_list_range: need rank_begin <= rank_end <= n");
+    const bool full = rank_begin == 0 && rank_end == n;
     tl_status st;
     ctx->launches = 0;  // this call's kernels; the last orient's are in orient_launches
     if (algo == TL_ALGO_APP) {
@@ -918,6 +950,8 @@ TL_API tl_status tl_list(tl_ctx* ctx, int algo, unsigned out_flags, tl_stats* ou
     base.acc = acc;
     base.vcount = want_vc ? P<unsigned long long>(ctx->vcount) : nullptr;
     base.variant = ctx->variant;
+    base.hot_rank = ctx->hot_rank;
+    base.hist_base = n > kHist ? n - kHist : 0;
     base.bm_shrink = ctx->bm_shrink;
 
     CK(cudaEventRecord(ctx->ev[PH_COUNT + 3], ctx->s));
@@ -925,9 +959,21 @@ TL_API tl_status tl_list(tl_ctx* ctx, int algo, unsigned out_flags, tl_stats* ou
     uint32_t* L = P<uint32_t>(ctx->lists);
     uint32_t* const lists[kClasses] = {L, L + n, L + 2 * (uint64_t)n, L + 3 * (uint64_t)n, L + 4 * (uint64_t)n};
     SeedLists SL{{lists[0], lists[1], lists[2], lists[3], lists[4]}, counts};
-    if (n) {
-        k_classify_seeds<<<grid_for(n, 256, ctx->sms * 16), 256, 0, ctx->s>>>(n, base.set_len, SL);
+    if (rank_end > rank_begin) {
+        k_classify_seeds<<<grid_for(rank_end - rank_begin, 256, ctx->sms * 16), 256, 0, ctx->s>>>(
+            rank_begin, rank_end, base.set_len, SL);
         LAUNCHED();
+    }
+    unsigned long long range_ops[2] = {0, 0};  // inner_ops, mark_ops of a partial range
+    if (!full) {
+        auto* rc = reinterpret_cast<unsigned long long*>(counts + 16);  // small[64..80)
+        CK(cudaMemsetAsync(rc, 0, 16, ctx->s));
+        if (rank_end > rank_begin) {
+            k_range_cost<<<grid_for((uint64_t)(rank_end - rank_begin) * 32, 256, ctx->sms * 16), 256, 0, ctx->s>>>(
+                rank_begin, rank_end, base.set_off, base.set_len, base.set_adj, base.out_len, rc);
+            LAUNCHED();
+        }
+        CK(cudaMemcpyAsync(range_ops, rc, 16, cudaMemcpyDeviceToHost, ctx->s));
     }
     CK(cudaEventRecord(ctx->ev[PH_CLASSIFY], ctx->s));
     unsigned h[kClasses];
@@ -945,20 +991,38 @@ TL_API tl_status tl_list(tl_ctx* ctx, int algo, unsigned out_flags, tl_stats* ou
     };
     unsigned long long res[3] = {0, 0, 0};
     if (want_list) {
-        // pass 1 counts, so the triangle buffer is sized exactly
-        st = run(0);
-        if (st != TL_OK) return st;
-        CK(cudaMemcpyAsync(res, acc, 8, cudaMemcpyDeviceToHost, ctx->s));
-        CK(cudaStreamSynchronize(ctx->s));
-        ENSURE(tri, (size_t)std::max<unsigned long long>(res[0], 1) * 12);
+        // One pass into the context's triangle buffer (grow-only, kept across
+        // calls): the cursor counts every triangle, writes stop at capacity.
+        // Only when the list outgrows the buffer is it grown to the exact
+        // size and the pass repeated. First call: a quarter of the free
+        // device memory, at most 2^31 triangles.
+        if (ctx->tri.cap < 12 * 64) {
+            size_t free_b = 0, total_b = 0;
+            if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+                (void)cudaGetLastError();
+                free_b = 0;
+            }
+            const size_t want = std::min<size_t>(free_b / 4, (size_t{1} << 31) * 12);
+            ENSURE(tri, std::max<size_t>(want / 12 * 12, 12 * 64));
+        }
         base.tri = P<uint32_t>(ctx->tri);
-        base.tri_cap = res[0];
+        base.tri_cap = ctx->tri.cap / 12;
     }
     st = run(out_flags);
     if (st != TL_OK) return st;
-    CK(cudaEventRecord(ctx->ev[PH_LIST], ctx->s));
     CK(cudaMemcpyAsync(res, acc, sizeof(res), cudaMemcpyDeviceToHost, ctx->s));
     CK(cudaStreamSynchronize(ctx->s));
+    if (want_list && res[2] > base.tri_cap) {
+        ENSURE(tri, (size_t)res[2] * 12);
+        base.tri = P<uint32_t>(ctx->tri);
+        base.tri_cap = ctx->tri.cap / 12;
+        st = run(out_flags);
+        if (st != TL_OK) return st;
+        CK(cudaMemcpyAsync(res, acc, sizeof(res), cudaMemcpyDeviceToHost, ctx->s));
+        CK(cudaStreamSynchronize(ctx->s));
+    }
+    CK(cudaEventRecord(ctx->ev[PH_LIST], ctx->s));
+    CK(cudaEventSynchronize(ctx->ev[PH_LIST]));
     ctx->phase_ms[PH_CLASSIFY] = ev_ms(ctx->ev[PH_COUNT + 3], ctx->ev[PH_CLASSIFY]);
     ctx->phase_ms[PH_LIST] = ev_ms(ctx->ev[PH_COUNT + 4], ctx->ev[PH_LIST]);
     for (int c = 0; c < kClasses; ++c)
@@ -967,7 +1031,7 @@ TL_API tl_status tl_list(tl_ctx* ctx, int algo, unsigned out_flags, tl_stats* ou
     ctx->have_tri = want_list;
     ctx->tri_count = want_list ? res[2] : 0;
     if (want_list && res[2] != res[0])
-        return ctx->fail(TL_ERR_CUDA, "tl_list: list pass emitted a different number of triangles than the count pass");
+        return ctx->fail(TL_ERR_CUDA, "tl_list: the list cursor disagrees with the triangle count");
     if (out) {
         std::memset(out, 0, sizeof(*out));
         out->triangle_count = res[0];
@@ -976,8 +1040,8 @@ TL_API tl_status tl_list(tl_ctx* ctx, int algo, unsigned out_flags, tl_stats* ou
         out->c_pm = ctx->cost[1];
         out->c_mm = ctx->cost[2];
         out->sum_deg_sq = ctx->cost[3];
-        out->inner_ops = algo == TL_ALGO_APM ? ctx->cost[1] : ctx->cost[0];
-        out->mark_ops = 2 * ctx->m;
+        out->inner_ops = !full ? range_ops[0] : algo == TL_ALGO_APM ? ctx->cost[1] : ctx->cost[0];
+        out->mark_ops = !full ? range_ops[1] : 2 * ctx->m;
         out->orient_ms = ctx->orient_ms;
         out->list_ms = ev_ms(ctx->ev[PH_COUNT + 3], ctx->ev[PH_LIST]);
         out->h2d_ms = ctx->h2d_ms;

@@ -172,6 +172,12 @@ class Context:
         _check(self._p, _native.trigpu().tl_list(self._p, algo, flags, C.byref(st)))
         return st
 
+    def list_range(self, algo: int, flags: int, rank_begin: int, rank_end: int) -> TlStats:
+        """run_*_range (listing.hpp:69-107) over the seeds ranked [rank_begin, rank_end)."""
+        st = TlStats()
+        _check(self._p, _native.trigpu().tl_list_range(self._p, algo, flags, rank_begin, rank_end, C.byref(st)))
+        return st
+
     def fetch_triangles(self) -> np.ndarray:
         k = C.c_uint64(0)
         lib = _native.trigpu()

@@ -1,10 +1,11 @@
-"""A/B timing of the listing kernels on one config (experiments, not the bench).
+"""A/B timing of listing-kernel builds on one config (experiments, not the bench).
 
-    python tools/ab.py [--config c4] [--algo apm] [--flags 1] [--variant 0] [--reps 5]
+    python tools/ab.py [--config c4] [--libs base,_c1r4] [--flags 1] [--algo apm] [--reps 5]
 
-Select an experimental build with TRIGPU_LIB_SUFFIX. The ordering is computed
-on the device (tl_order, bit-identical to the reference's degree / split
-order). Prints one JSON line: mean per-phase device times over the reps.
+Generates the graph once; for each library variant (lib/libtrigpu<suffix>.so,
+"base" = lib/libtrigpu.so) orients, lists `reps` times and prints one JSON line
+of mean per-phase device times. The ordering is computed on the device
+(tl_order, bit-identical to the reference's degree / split order).
 """
 import argparse
 import json
@@ -14,39 +15,51 @@ import sys
 import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np  # noqa: E402
 
 import bench  # noqa: E402
 import paper_2203_04774_b200 as tg  # noqa: E402
+from paper_2203_04774_b200 import _native  # noqa: E402
 from paper_2203_04774_b200._native import TL_DEBUG_VARIANT  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c4")
 ap.add_argument("--ordering", default="degree")
 ap.add_argument("--algo", default="apm")
-ap.add_argument("--flags", type=int, default=1)
+ap.add_argument("--flags", default="1")
+ap.add_argument("--libs", default="base")
 ap.add_argument("--variant", type=int, default=0)
 ap.add_argument("--reps", type=int, default=5)
 a = ap.parse_args()
 t0 = time.perf_counter()
 g = bench.make_graph(bench.CONFIGS[a.config])
-ctx = tg.Context(0)
-rank = ctx.order(g.offsets, a.ordering)
 gen_s = time.perf_counter() - t0
-ctx.orient(g.offsets, g.adjacency, rank)
-if a.variant:
-    ctx.debug_set(TL_DEBUG_VARIANT, a.variant)
+ranks = None
 algo = 1 if a.algo == "apm" else 0
-st = ctx.list(algo, a.flags)
-ph = []
-for _ in range(a.reps):
-    st2 = ctx.list(algo, a.flags)
-    assert st2.triangle_count == st.triangle_count or a.variant
-    ph.append(ctx.phase_times())
-mean = {k: round(statistics.mean(p[k] for p in ph), 3) for k in ph[0] if k.startswith("list") or k == "classify"}
-C = st.inner_ops
-B = 4 * (C + 2 * g.m)
-print(json.dumps({"config": a.config, "ordering": a.ordering, "algo": a.algo, "flags": a.flags,
-                  "variant": a.variant, "lib": os.environ.get("TRIGPU_LIB_SUFFIX", ""),
-                  "T": st.triangle_count, "checksum": st.checksum, "C": C, "m": g.m,
-                  "frac": B / (mean["list"] / 1e3) / 6550.1e9, "gen_s": round(gen_s, 1), **mean}), flush=True)
+ref = None
+for lib in a.libs.split(","):
+    _native.use_library_variant("" if lib == "base" else lib)
+    ctx = tg.Context(0)
+    if ranks is None:
+        ranks = ctx.order(g.offsets, a.ordering)
+    ctx.orient(g.offsets, g.adjacency, ranks)
+    ctx.orient(g.offsets, g.adjacency, ranks)  # second call: buffers allocated, orient_ms is warm
+    if a.variant:
+        ctx.debug_set(TL_DEBUG_VARIANT, a.variant)
+    for flags in (int(f) for f in a.flags.split(",")):
+        st = ctx.list(algo, flags)
+        if ref is None:
+            ref = st.triangle_count
+        assert st.triangle_count == ref or a.variant, (lib, st.triangle_count, ref)
+        ph = []
+        for _ in range(a.reps):
+            st2 = ctx.list(algo, flags)
+            assert st2.triangle_count == st.triangle_count and st2.checksum == st.checksum
+            ph.append(ctx.phase_times())
+        mean = {k: round(statistics.mean(p[k] for p in ph), 3) for k in ph[0]
+                if k.startswith("list") or k in ("classify", "in_csr")}
+        B = 4 * (st.inner_ops + 2 * g.m)
+        print(json.dumps({"config": a.config, "ordering": a.ordering, "algo": a.algo, "flags": flags,
+                          "variant": a.variant, "lib": lib, "T": st.triangle_count, "checksum": st.checksum,
+                          "C": st.inner_ops, "m": g.m, "frac": round(B / (mean["list"] / 1e3) / 6550.1e9, 4),
+                          "orient_ms": round(st.orient_ms, 2), "gen_s": round(gen_s, 1), **mean}), flush=True)
+    ctx.close()
