@@ -180,9 +180,14 @@ TL_API const char* tl_phase_name(int i);
  *                       2^value so graphs small enough for the oracle take the
  *                       below-window (filter + exact verification) path;
  *   TL_DEBUG_VARIANT    probe variant of a -DTRIGPU_EXPERIMENTS build (2 = null
- *                       probe, timing only); ignored otherwise.
+ *                       probe, timing only); ignored otherwise;
+ *   TL_DEBUG_CLASS_WORK 1: each tl_list also reports the inner_ops of every
+ *                       seed class through tl_phase_times ("work_*", counts);
+ *   TL_DEBUG_H_WIDE_MIN_N  class-H seeds run on the CTA-per-seed kernel with a
+ *                       2^19 window when n exceeds this (default 2^25), so tests
+ *                       on small graphs can force that path with 0.
  * Settings persist for the context. */
-enum { TL_DEBUG_BM_SHRINK = 1, TL_DEBUG_VARIANT = 2 };
+enum { TL_DEBUG_BM_SHRINK = 1, TL_DEBUG_VARIANT = 2, TL_DEBUG_CLASS_WORK = 3, TL_DEBUG_H_WIDE_MIN_N = 4 };
 TL_API tl_status tl_debug_set(tl_ctx* ctx, int key, int value);
 
 #ifdef __cplusplus

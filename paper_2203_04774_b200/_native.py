@@ -37,6 +37,8 @@ TL_OUT_VERTEX_COUNTS = 2
 TL_OUT_LIST = 4
 TL_DEBUG_BM_SHRINK = 1
 TL_DEBUG_VARIANT = 2
+TL_DEBUG_CLASS_WORK = 3
+TL_DEBUG_H_WIDE_MIN_N = 4
 
 # every exported symbol of include/trigpu.h (tests check the .so exports all)
 TRIGPU_SYMBOLS = (
@@ -186,6 +188,12 @@ def trihost() -> C.CDLL:
     lib.th_graph_new.restype = _vp
     lib.th_graph_free.argtypes = [_vp]
     lib.th_graph_free.restype = None
+    lib.th_graph_load.argtypes = [C.c_char_p, C.POINTER(_u64), C.POINTER(_u64)]
+    lib.th_graph_load.restype = _vp
+    lib.th_graph_to_csr.argtypes = [_vp, P]
+    lib.th_graph_to_csr.restype = C.c_int
+    lib.th_graph_labels.argtypes = [_vp, _vp]
+    lib.th_graph_labels.restype = None
     lib.th_order.argtypes = [_vp, C.c_char_p, _u64, _vp, C.POINTER(C.c_double)]
     lib.th_order.restype = C.c_int
     lib.th_cost.argtypes = [_vp, _vp, _vp]

@@ -65,6 +65,14 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
 __device__ __forceinline__ unsigned smem_addr(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
+// Shared address of the 32-bit word holding bit o of a bitmap at `base`:
+// base + (o >> 5) * 4 as SHF + LEA (written as mad so ptxas does not turn it
+// into SHF + LOP3 + IADD).
+__device__ __forceinline__ unsigned bit_word(unsigned base, uint32_t o) {
+    unsigned a;
+    asm("{\n\t.reg .u32 w;\n\tshr.u32 w, %1, 5;\n\tmad.lo.u32 %0, w, 4, %2;\n\t}" : "=r"(a) : "r"(o), "r"(base));
+    return a;
+}
 __device__ __forceinline__ uint4 lds128(unsigned a) {
     uint4 v;
     asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));

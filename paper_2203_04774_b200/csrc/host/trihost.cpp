@@ -416,6 +416,28 @@ void* th_graph_new(const th_csr* g) {
 
 void th_graph_free(void* graph) { delete static_cast<trilist::Graph*>(graph); }
 
+void* th_graph_load(const char* path, std::uint64_t* loops, std::uint64_t* dups) {
+    try {
+        trilist::NormalizeStats stats;
+        auto* g = new trilist::Graph(trilist::load_edgelist_file(path, &stats));
+        if (loops) *loops = stats.loops_removed;
+        if (dups) *dups = stats.duplicates_removed;
+        return g;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+
+int th_graph_to_csr(void* graph, th_csr* out) {
+    return csr_from_graph(*static_cast<trilist::Graph*>(graph), out);
+}
+
+void th_graph_labels(void* graph, std::int64_t* out) {
+    const auto& labels = static_cast<trilist::Graph*>(graph)->labels();
+    std::copy(labels.begin(), labels.end(), out);
+}
+
 int th_order(void* graph, const char* method, std::uint64_t seed, std::uint32_t* rank_out,
              double* order_ms) {
     try {

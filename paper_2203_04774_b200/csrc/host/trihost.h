@@ -48,6 +48,13 @@ int th_csr_check(const th_csr* g);
 /* Reference Graph handle (trilist::Graph built by from_dense_edges). */
 void* th_graph_new(const th_csr* g);
 void th_graph_free(void* graph);
+/* The reference's text loader (load_edgelist_file, graph.cpp:164-192: one
+ * "a b" label pair per line, '#' / '%' comments, normalize()). The handle
+ * works with th_order / th_cost; th_graph_to_csr copies its CSR out,
+ * th_graph_labels its labels (int64[n], dense id -> original label). */
+void* th_graph_load(const char* path, uint64_t* loops_removed, uint64_t* duplicates_removed);
+int th_graph_to_csr(void* graph, th_csr* out);
+void th_graph_labels(void* graph, int64_t* out);
 /* Ordering by reference method name: identity random degree core split check
  * neigh (trilist_cli.cpp:47-64). rank_out[v] = 0-based position of v. */
 int th_order(void* graph, const char* method, uint64_t seed, uint32_t* rank_out,

@@ -97,13 +97,13 @@ struct WinProbe {
     // 0/1: y is in S (y inside the window) / 0 (y outside)
     __device__ __forceinline__ uint32_t bit(uint32_t y) const {
         const uint32_t o = min(y - wb, la);
-        return (lds32(bm + ((o >> 5) << 2)) >> (o & 31u)) & 1u;
+        return (lds32(bit_word(bm, o)) >> (o & 31u)) & 1u;
     }
     __device__ __forceinline__ bool below(uint32_t y) const { return y < wb; }
     // region-B candidate (call for y below the window only)
     __device__ __forceinline__ uint32_t cand(uint32_t y) const {
         const uint32_t o = y & maskb;
-        return (lds32(bmb + ((o >> 5) << 2)) >> (o & 31u)) & 1u;
+        return (lds32(bit_word(bmb, o)) >> (o & 31u)) & 1u;
     }
     __device__ __forceinline__ bool verify(uint32_t y, bool act) const { return ver(y, act); }
     // the value padding a partial quad: never in the window, never below it
@@ -632,15 +632,9 @@ struct CtaRowCursor {
 //      element f of the concatenated rows; the owning row of each lane comes
 //      from an OR-reduction of the row starts), so short rows do not idle lanes.
 template <int ALGO, unsigned F, class Probe>
-__device__ __forceinline__ void scan_rows(const ListParams& P, uint32_t seed, uint32_t x, bool xvalid,
-                                          const Probe& probe, Sink<ALGO, F>& sink) {
+__device__ __forceinline__ void scan_rows_at(const ListParams& P, uint32_t seed, uint32_t x, uint64_t ro, uint32_t rl,
+                                             const Probe& probe, Sink<ALGO, F>& sink) {
     const unsigned lane = lane_id();
-    uint64_t ro = 0;
-    uint32_t rl = 0;
-    if (xvalid) {
-        ro = P.out_off[x];
-        rl = P.out_len[x];
-    }
     unsigned hits = 0;
     // ---- phase 1: long rows, quad chunks
     {
@@ -702,6 +696,18 @@ __device__ __forceinline__ void scan_rows(const ListParams& P, uint32_t seed, ui
         }
     }
     sink.cnt += hits;
+}
+
+template <int ALGO, unsigned F, class Probe>
+__device__ __forceinline__ void scan_rows(const ListParams& P, uint32_t seed, uint32_t x, bool xvalid,
+                                          const Probe& probe, Sink<ALGO, F>& sink) {
+    uint64_t ro = 0;
+    uint32_t rl = 0;
+    if (xvalid) {
+        ro = P.out_off[x];
+        rl = P.out_len[x];
+    }
+    scan_rows_at<ALGO, F>(P, seed, x, ro, rl, probe, sink);
 }
 
 // Chunks of 32 x's: set elements c, c + stride, ... below xe of the seed row at so.
@@ -777,25 +783,6 @@ __device__ __forceinline__ void flush_hist(const ListParams& P, const Sink<ALGO,
 #endif
 #define WARP_MINB(F) ((F) == 0u ? TRIGPU_WARP_MINB : TRIGPU_WARP_MINB_SINK)
 
-// Seeds handed to a warp in runs of G queue slots per atomic (one atomic per
-// seed on a single counter serialises at its L2 slice when seeds are tiny).
-template <unsigned G>
-struct WarpSeedQueue {
-    unsigned next = 0, end = 0;
-    __device__ __forceinline__ bool pop(const ListParams& P, unsigned& i) {
-        if (next == end) {
-            unsigned b = 0;
-            if (lane_id() == 0) b = atomicAdd(P.queue, G);
-            b = __shfl_sync(FULL, b, 0);
-            if (b >= P.nseeds) return false;
-            next = b;
-            end = min(b + G, P.nseeds);
-        }
-        i = next++;
-        return true;
-    }
-};
-
 // ---- class R: |S| <= 32, warp per seed --------------------------------------
 constexpr int kRWarps = 8;
 #ifndef TRIGPU_R_BITS_A
@@ -814,23 +801,65 @@ __global__ void __launch_bounds__(kRWarps * 32, TRIGPU_WARP_MINB) k_list_reg(Lis
     __syncwarp();
     Sink<ALGO, F> sink;
     attach_scratch(sink, dsm);
-    WarpSeedQueue<16> q;
-    for (unsigned i; q.pop(P, i);) {
-        const uint32_t seed = P.seeds[i];
-        sink.begin_unit(P, seed);
-        const uint64_t so = P.set_off[seed];
-        const uint32_t d = P.set_len[seed];
-        const uint32_t s = lane < d ? __ldg(P.set_adj + so + lane) : kNone;
-        const WinGeom g = win_geom(kRBitsA, kRBitsB, P.bm_shrink, __shfl_sync(FULL, s, 0), __shfl_sync(FULL, s, d - 1));
-        if (lane < d) win_set(bma, bmb, g, s);
-        __syncwarp();
-        with_win_probe(P, smem_addr(bma), smem_addr(bmb), g, RegVerify{s}, [&](const auto& probe) {
-            scan_rows<ALGO, F>(P, seed, s, lane < d, probe, sink);
-        });
-        sink.end_unit(P, seed);
-        __syncwarp();
-        if (lane < d) win_clear(bma, bmb, g, s);
-        __syncwarp();
+    // Seeds come in runs of 32 (one queue atomic); a run's seed ids, set rows
+    // and sizes are loaded lane-parallel at once, and each seed's set (and
+    // the offsets of its rows) is prefetched while the previous seed is
+    // listed, so a seed waits on one dependent round trip (its rows) instead
+    // of five. Tiny seeds are latency-bound, not bandwidth-bound.
+    for (;;) {
+        unsigned b = 0;
+        if (lane == 0) b = atomicAdd(P.queue, 32u);
+        b = __shfl_sync(FULL, b, 0);
+        if (b >= P.nseeds) break;
+        const unsigned cnt = min(32u, P.nseeds - b);
+        uint32_t seed_l = 0, d_l = 0;
+        uint64_t so_l = 0;
+        if (lane < cnt) {
+            seed_l = P.seeds[b + lane];
+            so_l = P.set_off[seed_l];
+            d_l = P.set_len[seed_l];
+        }
+        // seed 0's set and row offsets
+        uint32_t d = __shfl_sync(FULL, d_l, 0);
+        uint64_t so = shfl64(so_l, 0);
+        uint32_t s = lane < d ? __ldg(P.set_adj + so + lane) : kNone;
+        uint64_t ro = 0;
+        uint32_t rl = 0;
+        if (lane < d) {
+            ro = P.out_off[s];
+            rl = P.out_len[s];
+        }
+        for (unsigned k = 0; k < cnt; ++k) {
+            const uint32_t seed = __shfl_sync(FULL, seed_l, k);
+            // prefetch the next seed's set
+            uint32_t d1 = 0, s1 = kNone;
+            if (k + 1 < cnt) {
+                d1 = __shfl_sync(FULL, d_l, k + 1);
+                const uint64_t so1 = shfl64(so_l, k + 1);
+                if (lane < d1) s1 = __ldg(P.set_adj + so1 + lane);
+            }
+            sink.begin_unit(P, seed);
+            const WinGeom g =
+                win_geom(kRBitsA, kRBitsB, P.bm_shrink, __shfl_sync(FULL, s, 0), __shfl_sync(FULL, s, d - 1));
+            if (lane < d) win_set(bma, bmb, g, s);
+            __syncwarp();
+            with_win_probe(P, smem_addr(bma), smem_addr(bmb), g, RegVerify{s}, [&](const auto& probe) {
+                scan_rows_at<ALGO, F>(P, seed, s, ro, rl, probe, sink);
+            });
+            sink.end_unit(P, seed);
+            __syncwarp();
+            if (lane < d) win_clear(bma, bmb, g, s);
+            __syncwarp();
+            // the next seed's row offsets (its set has arrived by now)
+            d = d1;
+            s = s1;
+            ro = 0;
+            rl = 0;
+            if (lane < d) {
+                ro = P.out_off[s];
+                rl = P.out_len[s];
+            }
+        }
     }
     sink.flush(P);
     flush_hist(P, sink);
@@ -921,8 +950,17 @@ struct CtaCfg {
 #define TRIGPU_H_BITS_A_CTA 17
 #endif
 using CfgC1 = CtaCfg<256, TRIGPU_C1_BITS_A, 14, 1024, TRIGPU_C1_MINB, TRIGPU_C1_RING>;  // (2^17 window at 4 CTAs/SM: C4 -1 %, C5 +4 %)
-using CfgC2 = CtaCfg<1024, 19, 15, 4096, 1, TRIGPU_C2_RING>;  // (2 x 512-thread CTAs, 2^18 window: C5 5 % slower)
+#ifndef TRIGPU_C2_BITS_A
+#define TRIGPU_C2_BITS_A 19
+#endif
+using CfgC2 = CtaCfg<1024, TRIGPU_C2_BITS_A, 15, 4096, 1, TRIGPU_C2_RING>;  // (2 x 512-thread CTAs, 2^18 window: C5 5 % slower)
 using CfgH = CtaCfg<256, TRIGPU_H_BITS_A_CTA, 13, 256, TRIGPU_H_MINB, TRIGPU_H_RING>;
+// Class H on graphs of more than 2^25 vertices: the set of an H seed spans so
+// many ranks that the per-warp 2^16 window leaves many of its elements to the
+// filter + verification path; a CTA per seed shares one 2^19 window
+// (measured on C5: H 1275 -> 1147 ms; on C4 the warp kernel stays faster).
+using CfgHWide = CtaCfg<256, 19, 13, 256, 3, 0>;
+constexpr uint32_t kHWideMinN = 1u << 25;
 template <class CFG>
 constexpr size_t cta_bitmap_bytes() { return win_bytes(CFG::kBitsA, CFG::kBitsB); }
 template <class CFG>
@@ -1106,7 +1144,7 @@ struct WinGlobalProbe {
     const uint32_t* gbm;  // exact global bitmap of the set's elements below wb
     __device__ __forceinline__ uint32_t bit(uint32_t y) const {
         const uint32_t o = min(y - wb, la);
-        return (lds32(bm + ((o >> 5) << 2)) >> (o & 31u)) & 1u;
+        return (lds32(bit_word(bm, o)) >> (o & 31u)) & 1u;
     }
     __device__ __forceinline__ bool below(uint32_t y) const { return y < wb; }
     __device__ __forceinline__ uint32_t cand(uint32_t y) const { return (__ldcg(gbm + (y >> 5)) >> (y & 31u)) & 1u; }
@@ -1197,6 +1235,27 @@ __global__ void __launch_bounds__(256) k_classify_seeds(uint32_t rb, uint32_t re
             if (cls == c) L.lists[c][base + __popc(b & lanemask_lt())] = (uint32_t)r;
         }
     }
+}
+
+// Per-class inner_ops (TL_DEBUG_CLASS_WORK): work[c] += sum over x in set(s)
+// of d+(x) for every seed s of class c. Warp per seed of one class list.
+__global__ void __launch_bounds__(256) k_class_work(const uint32_t* __restrict__ seeds, unsigned nseeds,
+                                                   const uint64_t* __restrict__ set_off,
+                                                   const uint32_t* __restrict__ set_len,
+                                                   const uint32_t* __restrict__ set_adj,
+                                                   const uint32_t* __restrict__ out_len,
+                                                   unsigned long long* __restrict__ work) {
+    const unsigned lane = lane_id();
+    const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    unsigned long long w = 0;
+    for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; i < nseeds; i += warps) {
+        const uint32_t r = seeds[i];
+        const uint64_t so = set_off[r];
+        const uint32_t d = set_len[r];
+        for (uint32_t k = lane; k < d; k += 32) w += out_len[set_adj[so + k]];
+    }
+    w = warp_sum64(w);
+    if (lane == 0 && w) atomicAdd(work, w);
 }
 
 // inner_ops / mark_ops of the seeds in [rb, re) (tl_list_range): per seed s,

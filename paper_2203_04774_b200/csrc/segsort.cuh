@@ -5,8 +5,12 @@
 // rows in dense-id order, so every row is sorted here. Values in a row are
 // distinct ranks (simple graph), which the bitmap path relies on. Size classes:
 //   L <= 16            thread per row, bitonic network in registers
-//   16 < L <= 256      warp per row, cub::WarpMergeSort (8 keys / lane)
-//   256 < L <= 4096    CTA per row, cub::BlockRadixSort (16 keys / thread)
+//   16 < L <= 32       16 lanes per row, cub::WarpMergeSort (2 keys / lane)
+//   32 < L <= 64       warp per row, cub::WarpMergeSort (2 keys / lane)
+//   64 < L <= 256      warp per row, cub::WarpMergeSort (8 keys / lane)
+//   256 < L <= 1024    CTA per row, cub::BlockRadixSort (4 keys / thread)
+//   1024 < L <= 4096   CTA per row, cub::BlockRadixSort (16 keys / thread)
+// (radix sorts use 6-bit digits over bits(n) + 1 key bits)
 //   L > 4096           CTA per row: bucket by 2^19-value window into a temp
 //                      row, then per window either BlockRadixSort (<= 2048
 //                      entries) or a 64 KB shared-memory bitmap + popc compaction
@@ -20,11 +24,10 @@
 
 namespace trigpu {
 
+enum : int { kSortW32 = 0, kSortW64, kSortW256, kSortB1K, kSortB4K, kSortBig, kSortClasses };
 struct SortLists {
-    uint32_t* warp_rows;
-    uint32_t* block_rows;
-    uint32_t* big_rows;
-    unsigned int* counts;  // [0] warp, [1] block, [2] big
+    uint32_t* rows[kSortClasses];  // row ids per size class
+    unsigned int* counts;          // [kSortClasses]
 };
 
 // Row r is adj[off[r], off[r] + L): L = len[r] when a length array is given
@@ -36,6 +39,10 @@ __device__ __forceinline__ uint64_t row_len(const uint64_t* off, const uint32_t*
 constexpr uint32_t kSortThreadMax = 16;
 constexpr uint32_t kSortWarpMax = 256;
 constexpr uint32_t kSortBlockMax = 4096;
+// upper bound of each listed class
+__device__ __forceinline__ uint32_t sort_class_max(int c) {
+    return c == 0 ? 32u : c == 1 ? 64u : c == 2 ? 256u : c == 3 ? 1024u : c == 4 ? 4096u : 0xFFFFFFFFu;
+}
 
 __device__ __forceinline__ void warp_append(uint32_t* list, unsigned int* count, bool pred, uint32_t v) {
     const unsigned b = __ballot_sync(FULL, pred);
@@ -84,9 +91,12 @@ __global__ void __launch_bounds__(256) k_sort_small(uint32_t n, const uint64_t* 
             for (int i = 0; i < (int)kSortThreadMax; ++i)
                 if ((uint64_t)i < L) p[i] = a[i];
         }
-        warp_append(lists.warp_rows, &lists.counts[0], L > kSortThreadMax && L <= kSortWarpMax, (uint32_t)r);
-        warp_append(lists.block_rows, &lists.counts[1], L > kSortWarpMax && L <= kSortBlockMax, (uint32_t)r);
-        warp_append(lists.big_rows, &lists.counts[2], L > kSortBlockMax, (uint32_t)r);
+        uint32_t lo = kSortThreadMax;
+#pragma unroll
+        for (int c = 0; c < kSortClasses; ++c) {
+            warp_append(lists.rows[c], &lists.counts[c], L > lo && L <= sort_class_max(c), (uint32_t)r);
+            lo = sort_class_max(c);
+        }
     }
 }
 
@@ -94,30 +104,40 @@ struct U32Less {
     __device__ __forceinline__ bool operator()(uint32_t a, uint32_t b) const { return a < b; }
 };
 
-constexpr int kWarpSortItems = kSortWarpMax / 32;
-
-__global__ void __launch_bounds__(256) k_sort_warp(const uint64_t* __restrict__ off, const uint32_t* __restrict__ len, uint32_t* __restrict__ adj,
-                                                   const uint32_t* __restrict__ rows,
+// Logical warp of LW lanes per row, ITEMS keys per lane (rows up to LW * ITEMS).
+template <int ITEMS, int LW>
+__global__ void __launch_bounds__(256) k_sort_warp(const uint64_t* __restrict__ off, const uint32_t* __restrict__ len,
+                                                   uint32_t* __restrict__ adj, const uint32_t* __restrict__ rows,
                                                    const unsigned int* __restrict__ count) {
-    using WS = cub::WarpMergeSort<uint32_t, kWarpSortItems, 32>;
-    __shared__ typename WS::TempStorage tmp[8];
-    const unsigned warp = threadIdx.x >> 5, lane = lane_id();
+    constexpr int kGroups = 256 / LW;
+    using WS = cub::WarpMergeSort<uint32_t, ITEMS, LW>;
+    __shared__ typename WS::TempStorage tmp[kGroups];
+    const unsigned grp = threadIdx.x / LW, gl = threadIdx.x % LW;
     const unsigned total = *count;
-    for (unsigned i = blockIdx.x * 8 + warp; i < total; i += gridDim.x * 8) {
-        const uint32_t r = rows[i];
-        const uint64_t b = off[r];
-        const int L = (int)row_len(off, len, r);
-        uint32_t* p = adj + b;
-        uint32_t k[kWarpSortItems];
+    // uniform trip count per physical warp (the logical warps of a warp stay converged)
+    const unsigned stride = gridDim.x * kGroups;
+    const unsigned first = blockIdx.x * kGroups + grp;
+    const unsigned warp_first = blockIdx.x * kGroups + (threadIdx.x / 32) * (32 / LW);
+    for (unsigned base = warp_first; base < total; base += stride) {
+        const unsigned i = first + (base - warp_first);
+        const bool act = i < total;
+        uint32_t* p = adj;
+        int L = 0;
+        if (act) {
+            const uint32_t r = rows[i];
+            p = adj + off[r];
+            L = (int)row_len(off, len, r);
+        }
+        uint32_t k[ITEMS];
 #pragma unroll
-        for (int j = 0; j < kWarpSortItems; ++j) {
-            const int idx = lane * kWarpSortItems + j;
+        for (int j = 0; j < ITEMS; ++j) {
+            const int idx = gl * ITEMS + j;
             k[j] = idx < L ? p[idx] : kNone;
         }
-        WS(tmp[warp]).Sort(k, U32Less(), L, kNone);
+        WS(tmp[grp]).Sort(k, U32Less(), L, kNone);
 #pragma unroll
-        for (int j = 0; j < kWarpSortItems; ++j) {
-            const int idx = lane * kWarpSortItems + j;
+        for (int j = 0; j < ITEMS; ++j) {
+            const int idx = gl * ITEMS + j;
             if (idx < L) p[idx] = k[j];
         }
         __syncwarp();
@@ -125,14 +145,15 @@ __global__ void __launch_bounds__(256) k_sort_warp(const uint64_t* __restrict__ 
 }
 
 constexpr int kBlockSortThreads = 256;
-constexpr int kBlockSortItems = kSortBlockMax / kBlockSortThreads;
+constexpr int kRadixBits = 6;
 
+template <int ITEMS>
 __global__ void __launch_bounds__(kBlockSortThreads) k_sort_block(const uint64_t* __restrict__ off, const uint32_t* __restrict__ len,
                                                                   uint32_t* __restrict__ adj,
                                                                   const uint32_t* __restrict__ rows,
                                                                   const unsigned int* __restrict__ count,
                                                                   int end_bit) {
-    using BRS = cub::BlockRadixSort<uint32_t, kBlockSortThreads, kBlockSortItems>;
+    using BRS = cub::BlockRadixSort<uint32_t, kBlockSortThreads, ITEMS, cub::NullType, kRadixBits>;
     __shared__ typename BRS::TempStorage tmp;
     const unsigned total = *count;
     for (unsigned i = blockIdx.x; i < total; i += gridDim.x) {
@@ -140,17 +161,17 @@ __global__ void __launch_bounds__(kBlockSortThreads) k_sort_block(const uint64_t
         const uint64_t b = off[r];
         const int L = (int)row_len(off, len, r);
         uint32_t* p = adj + b;
-        uint32_t k[kBlockSortItems];
+        uint32_t k[ITEMS];
         // blocked arrangement; padding (all ones) sorts last under end_bit > bits(n-1)
 #pragma unroll
-        for (int j = 0; j < kBlockSortItems; ++j) {
-            const int idx = threadIdx.x * kBlockSortItems + j;
+        for (int j = 0; j < ITEMS; ++j) {
+            const int idx = threadIdx.x * ITEMS + j;
             k[j] = idx < L ? p[idx] : kNone;
         }
         BRS(tmp).Sort(k, 0, end_bit);
 #pragma unroll
-        for (int j = 0; j < kBlockSortItems; ++j) {
-            const int idx = threadIdx.x * kBlockSortItems + j;
+        for (int j = 0; j < ITEMS; ++j) {
+            const int idx = threadIdx.x * ITEMS + j;
             if (idx < L) p[idx] = k[j];
         }
         __syncthreads();

@@ -61,11 +61,21 @@ enum Phase {
     PH_LIST_C1,
     PH_LIST_C2,
     PH_LIST_G,
+    PH_SORT_SMALL,  // segmented-sort classes of the last orientation's out-CSR
+    PH_SORT_WARP,
+    PH_SORT_BLOCK,
+    PH_SORT_BIG,
+    PH_WORK_R,  // per-class inner_ops of the last tl_list (TL_DEBUG_CLASS_WORK only; a count, not ms)
+    PH_WORK_H,
+    PH_WORK_C1,
+    PH_WORK_C2,
+    PH_WORK_G,
     PH_COUNT
 };
 const char* kPhaseNames[PH_COUNT] = {"h2d",    "relabel_count", "scan",    "scatter", "segsort", "cost",
                                      "in_csr", "classify",      "list",    "list_R",  "list_H",  "list_C1",
-                                     "list_C2", "list_G"};
+                                     "list_C2", "list_G", "sort_small", "sort_warp", "sort_block", "sort_big",
+                                     "work_R", "work_H", "work_C1", "work_C2", "work_G"};
 
 struct DevBuf {
     void* p = nullptr;
@@ -82,6 +92,8 @@ struct tl_ctx {
     cudaEvent_t timer0 = nullptr, timer1 = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
     cudaEvent_t cls_ev[10] = {};  // start / end of each seed-class launch
+    cudaEvent_t sort_ev[8] = {};  // start / end of the segmented-sort class kernels
+    bool sort_run[4] = {};
     bool cls_run[5] = {};
     std::string err;
     double phase_ms[PH_COUNT] = {};
@@ -104,6 +116,8 @@ struct tl_ctx {
     bool have_vcounts = false, have_tri = false;
     int variant = 0;         // TL_DEBUG_VARIANT: probe flavour of an experiments build (A/B timing)
     uint32_t bm_shrink = 0;  // TL_DEBUG_BM_SHRINK: smaller bitmaps (tests force the filter path)
+    bool class_work = false; // TL_DEBUG_CLASS_WORK: per-class inner_ops into the phase table
+    uint32_t h_wide_min_n = kHWideMinN;  // TL_DEBUG_H_WIDE_MIN_N: class H runs CTA-wide above this n
     unsigned long long tri_count = 0;
 
     tl_status fail(tl_status st, const std::string& what) {
@@ -184,36 +198,67 @@ tl_status scan_offsets(tl_ctx* ctx, uint32_t n, const uint32_t* cnt, uint64_t* o
     return TL_OK;
 }
 
-// Segmented sort of every row of (off, adj) in place; tmp has >= off[n] slots.
+// Segmented sort of every row of (off, adj) in place; tmp has >= off[n] slots
+// (the big-row buckets index it by the row offsets).
 tl_status sort_rows(tl_ctx* ctx, uint32_t n, uint64_t* off, const uint32_t* len, uint32_t* adj, uint32_t* tmp) {
     ENSURE(small, 128);
+    ENSURE(lists, (size_t)std::max<uint32_t>(n, 1) * 4 * std::max(kClasses, (int)kSortClasses));
     auto* counts = static_cast<unsigned int*>(ctx->small.p);
-    CK(cudaMemsetAsync(counts, 0, 4 * sizeof(unsigned int), ctx->s));
+    CK(cudaMemsetAsync(counts, 0, kSortClasses * sizeof(unsigned int), ctx->s));
     uint32_t* lists = P<uint32_t>(ctx->lists);
-    SortLists L{lists, lists + n, lists + 2 * (uint64_t)n, counts};
+    SortLists L{};
+    for (int c = 0; c < kSortClasses; ++c) L.rows[c] = lists + (uint64_t)c * n;
+    L.counts = counts;
+    CK(cudaEventRecord(ctx->sort_ev[0], ctx->s));
     k_sort_small<<<grid_for(n, 256, ctx->sms * 16), 256, 0, ctx->s>>>(n, off, len, adj, L);
     LAUNCHED();
-    unsigned int h[4];
+    CK(cudaEventRecord(ctx->sort_ev[1], ctx->s));
+    unsigned int h[kSortClasses];
     CK(cudaMemcpyAsync(h, counts, sizeof(h), cudaMemcpyDeviceToHost, ctx->s));
     CK(cudaStreamSynchronize(ctx->s));
     const int end_bit = std::min(32, (int)(32 - __builtin_clz(std::max(n, 2u) - 1)) + 1);
-    if (h[0]) {
-        k_sort_warp<<<grid_for((uint64_t)h[0] * 32, 256, ctx->sms * 8), 256, 0, ctx->s>>>(off, len, adj, L.warp_rows,
-                                                                                          counts + 0);
+    ctx->sort_run[0] = true;
+    ctx->sort_run[1] = h[kSortW32] || h[kSortW64] || h[kSortW256];
+    ctx->sort_run[2] = h[kSortB1K] || h[kSortB4K];
+    ctx->sort_run[3] = h[kSortBig] != 0;
+    CK(cudaEventRecord(ctx->sort_ev[2], ctx->s));
+    if (h[kSortW32]) {
+        k_sort_warp<2, 16><<<grid_for((uint64_t)h[kSortW32] * 16, 256, ctx->sms * 8), 256, 0, ctx->s>>>(
+            off, len, adj, L.rows[kSortW32], counts + kSortW32);
         LAUNCHED();
     }
-    if (h[1]) {
-        k_sort_block<<<std::min<unsigned>(h[1], ctx->sms * 8), kBlockSortThreads, 0, ctx->s>>>(
-            off, len, adj, L.block_rows, counts + 1, end_bit);
+    if (h[kSortW64]) {
+        k_sort_warp<2, 32><<<grid_for((uint64_t)h[kSortW64] * 32, 256, ctx->sms * 8), 256, 0, ctx->s>>>(
+            off, len, adj, L.rows[kSortW64], counts + kSortW64);
         LAUNCHED();
     }
-    if (h[2]) {
+    if (h[kSortW256]) {
+        k_sort_warp<8, 32><<<grid_for((uint64_t)h[kSortW256] * 32, 256, ctx->sms * 8), 256, 0, ctx->s>>>(
+            off, len, adj, L.rows[kSortW256], counts + kSortW256);
+        LAUNCHED();
+    }
+    CK(cudaEventRecord(ctx->sort_ev[3], ctx->s));
+    CK(cudaEventRecord(ctx->sort_ev[4], ctx->s));
+    if (h[kSortB1K]) {
+        k_sort_block<4><<<std::min<unsigned>(h[kSortB1K], ctx->sms * 8), kBlockSortThreads, 0, ctx->s>>>(
+            off, len, adj, L.rows[kSortB1K], counts + kSortB1K, end_bit);
+        LAUNCHED();
+    }
+    if (h[kSortB4K]) {
+        k_sort_block<16><<<std::min<unsigned>(h[kSortB4K], ctx->sms * 8), kBlockSortThreads, 0, ctx->s>>>(
+            off, len, adj, L.rows[kSortB4K], counts + kSortB4K, end_bit);
+        LAUNCHED();
+    }
+    CK(cudaEventRecord(ctx->sort_ev[5], ctx->s));
+    CK(cudaEventRecord(ctx->sort_ev[6], ctx->s));
+    if (h[kSortBig]) {
         const size_t smem = sizeof(BigSortSmem);
         CK(cudaFuncSetAttribute(k_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_sort_big<<<std::min<unsigned>(h[2], ctx->sms * 2), kBigThreads, smem, ctx->s>>>(n, off, len, adj, tmp,
-                                                                                       L.big_rows, counts + 2);
+        k_sort_big<<<std::min<unsigned>(h[kSortBig], ctx->sms * 2), kBigThreads, smem, ctx->s>>>(
+            n, off, len, adj, tmp, L.rows[kSortBig], counts + kSortBig);
         LAUNCHED();
     }
+    CK(cudaEventRecord(ctx->sort_ev[7], ctx->s));
     return TL_OK;
 }
 
@@ -345,6 +390,8 @@ tl_status orient_core(tl_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* goff,
     ctx->phase_ms[PH_SORT] = ev_ms(ctx->ev[PH_SCATTER], ctx->ev[PH_SORT]);
     ctx->phase_ms[PH_COST] = ev_ms(ctx->ev[PH_SORT], ctx->ev[PH_COST]);
     ctx->orient_ms = ev_ms(ctx->ev[PH_H2D], ctx->ev[PH_COST]);
+    for (int c = 0; c < 4; ++c)
+        ctx->phase_ms[PH_SORT_SMALL + c] = ctx->sort_run[c] ? ev_ms(ctx->sort_ev[2 * c], ctx->sort_ev[2 * c + 1]) : 0.0;
     ctx->orient_launches = ctx->launches;
     ctx->oriented = true;
     return TL_OK;
@@ -451,7 +498,10 @@ tl_status launch_classes(tl_ctx* ctx, ListParams base, uint32_t* const lists[kCl
         p.queue = queues + 4;
         const size_t smem = smem_giant<F>();
         if ((st = set_smem(ctx, k_list_giant<ALGO, F>, smem)) != TL_OK) return st;
-        const unsigned grid = std::min<unsigned>(h[4], (unsigned)ctx->sms);
+#ifndef TRIGPU_G_GRID
+#define TRIGPU_G_GRID 0  // CTAs for class G (0: one per SM)
+#endif
+        const unsigned grid = std::min<unsigned>(h[4], TRIGPU_G_GRID ? TRIGPU_G_GRID : (unsigned)ctx->sms);
         p.bitmap_words = ((uint64_t)ctx->n + 31) / 32 + 32;
         const size_t bm_bytes = (size_t)grid * p.bitmap_words * 4;
         if (ctx->bitmaps.cap < bm_bytes) {
@@ -491,6 +541,12 @@ tl_status launch_classes(tl_ctx* ctx, ListParams base, uint32_t* const lists[kCl
         if (st != TL_OK) return st;
         CK(cudaEventRecord(ctx->cls_ev[3], ctx->s));
 #else
+      if (ctx->n > ctx->h_wide_min_n) {
+        CK(cudaEventRecord(ctx->cls_ev[2], ctx->s));
+        st = launch_cta<ALGO, F, CfgHWide>(ctx, base, lists[1], h[1], queues + 1);
+        if (st != TL_OK) return st;
+        CK(cudaEventRecord(ctx->cls_ev[3], ctx->s));
+      } else {
         ListParams p = base;
         p.seeds = lists[1];
         p.nseeds = h[1];
@@ -503,6 +559,7 @@ tl_status launch_classes(tl_ctx* ctx, ListParams base, uint32_t* const lists[kCl
         k_list_warp<ALGO, F><<<grid, kHWarps * 32, smem, ctx->s>>>(p);
         LAUNCHED();
         CK(cudaEventRecord(ctx->cls_ev[3], ctx->s));
+      }
 #endif
         ctx->cls_run[1] = true;
     }
@@ -577,6 +634,7 @@ TL_API tl_status tl_create(tl_ctx** out, int device) {
     }
     for (auto& ev : ctx->ev) cudaEventCreate(&ev);
     for (auto& ev : ctx->cls_ev) cudaEventCreate(&ev);
+    for (auto& ev : ctx->sort_ev) cudaEventCreate(&ev);
     cudaEventCreateWithFlags(&ctx->fork, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ctx->join, cudaEventDisableTiming);
     *out = ctx;
@@ -596,6 +654,7 @@ TL_API void tl_destroy(tl_ctx* ctx) {
         if (b->p) cudaFree(b->p);
     for (auto& ev : ctx->ev) cudaEventDestroy(ev);
     for (auto& ev : ctx->cls_ev) cudaEventDestroy(ev);
+    for (auto& ev : ctx->sort_ev) cudaEventDestroy(ev);
     if (ctx->timer0) cudaEventDestroy(ctx->timer0);
     if (ctx->timer1) cudaEventDestroy(ctx->timer1);
     cudaEventDestroy(ctx->fork);
@@ -979,6 +1038,20 @@ TL_API tl_status tl_list_range(tl_ctx* ctx, int algo, unsigned out_flags, uint32
     unsigned h[kClasses];
     CK(cudaMemcpyAsync(h, counts, sizeof(h), cudaMemcpyDeviceToHost, ctx->s));
     CK(cudaStreamSynchronize(ctx->s));
+    if (ctx->class_work) {  // per-class inner_ops (debug; outside the timed listing)
+        auto* wk = reinterpret_cast<unsigned long long*>(counts + 20);  // small[80..120)
+        CK(cudaMemsetAsync(wk, 0, kClasses * 8, ctx->s));
+        for (int c = 0; c < kClasses; ++c)
+            if (h[c]) {
+                k_class_work<<<grid_for((uint64_t)h[c] * 32, 256, ctx->sms * 16), 256, 0, ctx->s>>>(
+                    lists[c], h[c], base.set_off, base.set_len, base.set_adj, base.out_len, wk + c);
+                LAUNCHED();
+            }
+        unsigned long long w[kClasses];
+        CK(cudaMemcpyAsync(w, wk, sizeof(w), cudaMemcpyDeviceToHost, ctx->s));
+        CK(cudaStreamSynchronize(ctx->s));
+        for (int c = 0; c < kClasses; ++c) ctx->phase_ms[PH_WORK_R + c] = static_cast<double>(w[c]);
+    }
 
     CK(cudaEventRecord(ctx->ev[PH_COUNT + 4], ctx->s));  // listing kernels start
     auto run = [&](unsigned F) -> tl_status {
@@ -1234,6 +1307,14 @@ TL_API tl_status tl_debug_set(tl_ctx* ctx, int key, int value) {
     }
     if (key == TL_DEBUG_VARIANT) {
         ctx->variant = value;
+        return TL_OK;
+    }
+    if (key == TL_DEBUG_CLASS_WORK) {
+        ctx->class_work = value != 0;
+        return TL_OK;
+    }
+    if (key == TL_DEBUG_H_WIDE_MIN_N) {
+        ctx->h_wide_min_n = static_cast<uint32_t>(value);
         return TL_OK;
     }
     return ctx->fail(TL_ERR_INVALID_ARGUMENT, "tl_debug_set: unknown key");

@@ -57,6 +57,32 @@ class Graph:
             raise HostError(_th_err())
         return cls._from_th(csr)
 
+    @classmethod
+    def load(cls, path: str) -> "Graph":
+        """load_edgelist_file (graph.cpp:164-192), the reference's own text
+        loader: label pairs, loops dropped, duplicates merged, labels re-indexed
+        densely in ascending order. ``labels`` / ``loops_removed`` /
+        ``duplicates_removed`` are set on the result."""
+        lo, du = C.c_uint64(0), C.c_uint64(0)
+        h = _native.trihost().th_graph_load(path.encode(), C.byref(lo), C.byref(du))
+        if not h:
+            raise HostError(_th_err())
+        ref = _RefGraph(h)
+        csr = _native.ThCsr()
+        if _native.trihost().th_graph_to_csr(h, C.byref(csr)) != 0:
+            raise HostError(_th_err())
+        g = cls._from_th(csr)
+        g._ref = ref
+        g.labels = np.zeros(max(g.n, 1), np.int64)
+        _native.trihost().th_graph_labels(h, g.labels.ctypes.data)
+        g.labels = g.labels[: g.n]
+        g.loops_removed, g.duplicates_removed = int(lo.value), int(du.value)
+        return g
+
+    def label_of(self, u: int) -> int:
+        labels = getattr(self, "labels", None)
+        return int(labels[u]) if labels is not None else int(u)
+
     # -- accessors (graph.hpp:31-43) -----------------------------------------
     def vertex_count(self) -> int:
         return int(self.offsets.shape[0] - 1)

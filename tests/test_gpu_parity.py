@@ -12,8 +12,8 @@ import pytest
 import oracle
 import paper_2203_04774_b200 as tg
 from paper_2203_04774_b200 import host
-from paper_2203_04774_b200._native import (TL_ALGO_APM, TL_ALGO_APP, TL_DEBUG_BM_SHRINK, TL_OUT_CHECKSUM,
-                                           TL_OUT_LIST, TL_OUT_VERTEX_COUNTS)
+from paper_2203_04774_b200._native import (TL_ALGO_APM, TL_ALGO_APP, TL_DEBUG_BM_SHRINK, TL_DEBUG_H_WIDE_MIN_N,
+                                           TL_OUT_CHECKSUM, TL_OUT_LIST, TL_OUT_VERTEX_COUNTS)
 from golden_io import case_csr, cases, golden, sha, sweep_graphs
 
 pytestmark = pytest.mark.gpu
@@ -292,6 +292,23 @@ def test_probe_filter_path(shrink):
         c.close()
 
 
+def test_wide_h_path():
+    """Class H on the CTA-per-seed 2^19-window kernel (the path graphs above
+    2^25 vertices take), forced on graphs the oracle checks in seconds, with
+    and without shrunken windows (filter + verification path)."""
+    c = tg.Context(0)
+    c.debug_set(TL_DEBUG_H_WIDE_MIN_N, 0)
+    try:
+        for shrink in (0, 6):
+            c.debug_set(TL_DEBUG_BM_SHRINK, shrink)
+            for g in (tg.gen_rmat(16, 16, 5), tg.gen_chung_lu(100000, 1600000, seed=6)):
+                for meth in ("degree", "split"):
+                    pi, _ = host.compute_order(g, meth)
+                    _oracle_check(c, g, pi, lists=(shrink == 0))
+    finally:
+        c.close()
+
+
 @pytest.mark.parametrize("meth", ["degree", "split"])
 def test_device_orderings_match_reference(meth):
     """tl_order (degree / split on the GPU) is bit-identical to the
@@ -388,3 +405,44 @@ def test_chunked_triangle_stream_with_labels():
         assert np.array_equal(got[np.lexsort(got.T[::-1])], exp_lab[np.lexsort(exp_lab.T[::-1])])
     finally:
         c.close()
+
+
+def test_cli_list_and_bench(tmp_path, capsys):
+    """The reference CLI's list / bench (trilist_cli.cpp:101-256) over the GPU:
+    cli_test.cpp's toy graph gives one triangle and the --out line "0 1 2";
+    relabelled inputs come back as their original labels; rows follow the
+    reference BenchRecord schema."""
+    from paper_2203_04774_b200 import cli
+    toy = tmp_path / "toy.txt"
+    toy.write_text("0 1\n0 2\n1 2\n2 3\n")
+    out = tmp_path / "tri.txt"
+    assert cli.main(["list", str(toy), "--out", str(out)]) == 0
+    text = capsys.readouterr().out.splitlines()
+    assert text[0] == "# sink collect" and text[1] == host.bench_csv_header()
+    row = text[2].split(",")
+    assert row[0] == "toy" and row[1] == "apm" and row[10] == "1"
+    assert out.read_text() == "0 1 2\n"
+    # labelled input with loops / duplicates, every ordering, both algorithms
+    rng = np.random.default_rng(4)
+    g = tg.gen_gnm(300, 2500, 5)
+    lab = rng.permutation(np.arange(300, dtype=np.int64) * 37 + 1000)
+    e = np.stack([np.repeat(np.arange(g.n), np.diff(g.offsets.astype(np.int64))), g.adjacency], 1)
+    lines = [f"{lab[a]} {lab[b]}" for a, b in e[::3]] + ["5000 5000"]
+    src = tmp_path / "lab.txt"
+    src.write_text("\n".join(lines) + "\n")
+    rg, _, _ = oracle.RefGraph.normalize(np.array([[int(x) for x in l.split()] for l in lines], np.int64))
+    for meth in ("degree", "core", "neigh"):
+        for algo in ("app", "apm"):
+            out2 = tmp_path / f"t_{meth}_{algo}.txt"
+            assert cli.main(["list", str(src), "--order", meth, "--algo", algo, "--out", str(out2)]) == 0
+            got = np.array([[int(x) for x in l.split()] for l in out2.read_text().splitlines()], np.int64)
+            exp = rg.labels()[rg.brute()]
+            assert got.shape == exp.shape
+            g_sorted = np.sort(got, axis=1)
+            assert np.array_equal(g_sorted[np.lexsort(g_sorted.T[::-1])],
+                                  np.sort(exp, axis=1)[np.lexsort(np.sort(exp, axis=1).T[::-1])])
+    capsys.readouterr()
+    assert cli.main(["bench", str(src), "--orderings", "degree,split", "--algos", "app,apm"]) == 0
+    rows = capsys.readouterr().out.splitlines()
+    assert rows[0] == host.bench_csv_header() and len(rows) == 5
+    assert len({r.split(",")[10] for r in rows[1:]}) == 1  # same triangle count every run

@@ -19,7 +19,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
 import paper_2203_04774_b200 as tg  # noqa: E402
 from paper_2203_04774_b200 import _native  # noqa: E402
-from paper_2203_04774_b200._native import TL_DEBUG_VARIANT  # noqa: E402
+from paper_2203_04774_b200._native import TL_DEBUG_CLASS_WORK, TL_DEBUG_VARIANT  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c4")
@@ -29,6 +29,7 @@ ap.add_argument("--flags", default="1")
 ap.add_argument("--libs", default="base")
 ap.add_argument("--variant", type=int, default=0)
 ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--class-work", action="store_true", help="report per-class inner_ops and GB/s")
 a = ap.parse_args()
 t0 = time.perf_counter()
 g = bench.make_graph(bench.CONFIGS[a.config])
@@ -45,6 +46,8 @@ for lib in a.libs.split(","):
     ctx.orient(g.offsets, g.adjacency, ranks)  # second call: buffers allocated, orient_ms is warm
     if a.variant:
         ctx.debug_set(TL_DEBUG_VARIANT, a.variant)
+    if a.class_work:
+        ctx.debug_set(TL_DEBUG_CLASS_WORK, 1)
     for flags in (int(f) for f in a.flags.split(",")):
         st = ctx.list(algo, flags)
         if ref is None:
@@ -56,7 +59,13 @@ for lib in a.libs.split(","):
             assert st2.triangle_count == st.triangle_count and st2.checksum == st.checksum
             ph.append(ctx.phase_times())
         mean = {k: round(statistics.mean(p[k] for p in ph), 3) for k in ph[0]
-                if k.startswith("list") or k in ("classify", "in_csr")}
+                if k.startswith("list") or k.startswith("sort_") or k in ("classify", "in_csr")}
+        if a.class_work:
+            for c in ("R", "H", "C1", "C2", "G"):
+                w = ph[-1]["work_" + c]
+                mean["work_" + c] = int(w)
+                if mean["list_" + c] > 0:
+                    mean["gbs_" + c] = round(4 * w / (mean["list_" + c] / 1e3) / 1e9, 1)
         B = 4 * (st.inner_ops + 2 * g.m)
         print(json.dumps({"config": a.config, "ordering": a.ordering, "algo": a.algo, "flags": flags,
                           "variant": a.variant, "lib": lib, "T": st.triangle_count, "checksum": st.checksum,
