@@ -46,10 +46,12 @@ struct ListParams {
     const uint32_t* out_adj;
     const uint32_t* inv;      // rank -> dense id
     const unsigned long long* hv;  // rank -> vertex_hash(dense id) (checksum sink)
-    unsigned long long* acc;  // [0] triangles, [1] checksum, [2] list cursor
+    unsigned long long* acc;  // [0] triangles, [1] checksum, [2] list chunk cursor, [3] list holes
     unsigned long long* vcount;  // rank space
     uint32_t* tri;
     unsigned long long tri_cap;
+    ulonglong2* holes;        // unused tails of the warps' last list chunks {start, length}
+    unsigned holes_cap;
     const uint32_t* seeds;    // class list
     unsigned int nseeds;
     unsigned int* queue;      // dynamic work counter
@@ -66,6 +68,7 @@ struct ListParams {
 // every lane busy (dense-id gathers, atomics) instead of with the 1-3 lanes
 // that hit in a batch.
 constexpr int kHitBuf = 96;  // 31 pending + up to 2 batches of 32 before a drain
+constexpr unsigned kListChunk = 1024;  // list slots a warp claims per global atomic
 
 // ---- the probe: a windowed bitmap over the seed's set ----------------------
 // S (sorted ranks s_0 < ... < s_{d-1}) is held in shared memory as
@@ -218,6 +221,7 @@ struct Sink {
     unsigned seed_hits = 0;
     unsigned buf = 0;      // shared address of this warp's kHitBuf uint2 entries
     unsigned pending = 0;  // warp-uniform
+    unsigned long long lcur = 0, lend = 0;  // the warp's list chunk: next slot, end (warp-uniform)
     uint32_t* hist = nullptr;  // the CTA's kHist counters (F_VCOUNT)
 
     // c more triangles containing vertex v (rank)
@@ -267,11 +271,21 @@ struct Sink {
             const uint32_t ru = ALGO == ALGO_APM ? seed : x;
             const uint32_t rv = ALGO == ALGO_APM ? x : y;
             const uint32_t rw = ALGO == ALGO_APM ? y : seed;
-            unsigned long long base = 0;
-            if (lane == 0) base = atomicAdd(&P.acc[2], (unsigned long long)n);
-            base = __shfl_sync(FULL, base, 0);
+            // slots from the warp's own chunk of kListChunk, a new chunk (one
+            // global atomic) when it runs out; a batch may straddle two chunks
+            const unsigned long long base0 = lcur;
+            const unsigned r = static_cast<unsigned>(min(lend - lcur, (unsigned long long)n));
+            unsigned long long base1 = 0;
+            if (r < n) {
+                if (lane == 0) base1 = atomicAdd(&P.acc[2], (unsigned long long)kListChunk);
+                base1 = __shfl_sync(FULL, base1, 0);
+                lcur = base1 + (n - r);
+                lend = base1 + kListChunk;
+            } else {
+                lcur += n;
+            }
             if (hit) {
-                const unsigned long long k = base + lane;
+                const unsigned long long k = lane < r ? base0 + lane : base1 + (lane - r);
                 if (k < P.tri_cap) {
                     P.tri[3 * k] = __ldg(P.inv + ru);
                     P.tri[3 * k + 1] = __ldg(P.inv + rv);
@@ -318,6 +332,14 @@ struct Sink {
     }
 
     __device__ __forceinline__ void flush(const ListParams& P) {
+        if constexpr ((F & F_LIST) != 0u) {
+            // the unused tail of the last chunk: recorded, filled after the
+            // listing by moving triangles from the end (tl_list)
+            if (lane_id() == 0 && lend > lcur) {
+                const unsigned long long h = atomicAdd(&P.acc[3], 1ull);
+                if (h < P.holes_cap) P.holes[h] = make_ulonglong2(lcur, lend - lcur);
+            }
+        }
         const unsigned long long c = warp_sum64(cnt);
         if (lane_id() == 0 && c) atomicAdd(&P.acc[0], c);
         if constexpr ((F & F_CHECKSUM) != 0u) {
@@ -782,22 +804,65 @@ __device__ __forceinline__ void flush_hist(const ListParams& P, const Sink<ALGO,
 #define TRIGPU_WARP_MINB_SINK 3
 #endif
 #define WARP_MINB(F) ((F) == 0u ? TRIGPU_WARP_MINB : TRIGPU_WARP_MINB_SINK)
+#ifndef TRIGPU_R_MINB_SINK
+#define TRIGPU_R_MINB_SINK TRIGPU_WARP_MINB
+#endif
+#define R_MINB(F) ((F) == 0u ? TRIGPU_WARP_MINB : TRIGPU_R_MINB_SINK)
 
 // ---- class R: |S| <= 32, warp per seed --------------------------------------
+// The set of an R seed (<= 32 ranks) may span the whole rank range (e.g. on a
+// Watts-Strogatz graph, where ranks are nearly unrelated to ring position), so
+// a rank window would leave most of it to the filter + verification path. A
+// per-warp open-addressing table of kRSlots keys (load <= 1/4, linear probing)
+// answers every probe exactly with ~1 LDS, wherever the set lies.
+constexpr uint32_t kRSlotBits = 7;
+constexpr uint32_t kRSlots = 1u << kRSlotBits;
+constexpr uint32_t kREmpty = 0xFFFFFFFEu;  // never a rank (and != kNone, the row pad)
+__device__ __forceinline__ uint32_t r_slot(uint32_t y) { return (y * 0x9E3779B1u) >> (32 - kRSlotBits); }
+struct HashProbe {
+    static constexpr bool low = false;
+    unsigned tab;  // shared address of the warp's kRSlots keys
+    __device__ __forceinline__ uint32_t bit(uint32_t y) const {
+        uint32_t h = r_slot(y);
+        uint32_t k = lds32(tab + 4u * h);
+        while (k != y && k != kREmpty) {
+            h = (h + 1u) & (kRSlots - 1u);
+            k = lds32(tab + 4u * h);
+        }
+        return k == y;
+    }
+    __device__ __forceinline__ bool below(uint32_t) const { return false; }
+    __device__ __forceinline__ uint32_t cand(uint32_t) const { return 0u; }
+    __device__ __forceinline__ bool verify(uint32_t, bool act) const { return act; }
+    __device__ __forceinline__ uint32_t sentinel() const { return kNone; }
+};
+// insert key s (a rank) into the table; returns its slot
+__device__ __forceinline__ uint32_t r_insert(uint32_t* tab, uint32_t s) {
+    uint32_t h = r_slot(s);
+    while (atomicCAS(tab + h, kREmpty, s) != kREmpty) h = (h + 1u) & (kRSlots - 1u);
+    return h;
+}
+#ifndef TRIGPU_R_HASH
+#define TRIGPU_R_HASH 0
+#endif
 constexpr int kRWarps = 8;
 #ifndef TRIGPU_R_BITS_A
 #define TRIGPU_R_BITS_A 15
 #endif
 constexpr uint32_t kRBitsA = TRIGPU_R_BITS_A, kRBitsB = 11;  // 4 KB window + 256 B region B per warp
+#if TRIGPU_R_HASH
+constexpr size_t kRBmBytes = kRSlots * 4;
+#else
 constexpr size_t kRBmBytes = win_bytes(kRBitsA, kRBitsB);
+#endif
 
 template <int ALGO, unsigned F>
-__global__ void __launch_bounds__(kRWarps * 32, TRIGPU_WARP_MINB) k_list_reg(ListParams P) {
+__global__ void __launch_bounds__(kRWarps * 32, R_MINB(F)) k_list_reg(ListParams P) {
     extern __shared__ __align__(16) unsigned char dsm[];
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
     uint32_t* bma = reinterpret_cast<uint32_t*>(dsm + warp_scratch_bytes<F>(kRWarps) + warp * kRBmBytes);
     uint32_t* bmb = bma + ((1u << kRBitsA) / 32 + 4);
-    for (uint32_t i = lane; i < kRBmBytes / 4; i += 32) bma[i] = 0u;
+    for (uint32_t i = lane; i < kRBmBytes / 4; i += 32) bma[i] = TRIGPU_R_HASH ? kREmpty : 0u;
     __syncwarp();
     Sink<ALGO, F> sink;
     attach_scratch(sink, dsm);
@@ -839,6 +904,16 @@ __global__ void __launch_bounds__(kRWarps * 32, TRIGPU_WARP_MINB) k_list_reg(Lis
                 if (lane < d1) s1 = __ldg(P.set_adj + so1 + lane);
             }
             sink.begin_unit(P, seed);
+#if TRIGPU_R_HASH
+            uint32_t slot = 0;
+            if (lane < d) slot = r_insert(bma, s);
+            __syncwarp();
+            scan_rows_at<ALGO, F>(P, seed, s, ro, rl, HashProbe{smem_addr(bma)}, sink);
+            sink.end_unit(P, seed);
+            __syncwarp();
+            if (lane < d) bma[slot] = kREmpty;
+            __syncwarp();
+#else
             const WinGeom g =
                 win_geom(kRBitsA, kRBitsB, P.bm_shrink, __shfl_sync(FULL, s, 0), __shfl_sync(FULL, s, d - 1));
             if (lane < d) win_set(bma, bmb, g, s);
@@ -850,6 +925,7 @@ __global__ void __launch_bounds__(kRWarps * 32, TRIGPU_WARP_MINB) k_list_reg(Lis
             __syncwarp();
             if (lane < d) win_clear(bma, bmb, g, s);
             __syncwarp();
+#endif
             // the next seed's row offsets (its set has arrived by now)
             d = d1;
             s = s1;
@@ -1135,19 +1211,33 @@ constexpr int kGWarps = kGThreads / 32;
 #define TRIGPU_G_BITS_A 20
 #endif
 constexpr uint32_t kGBitsA = TRIGPU_G_BITS_A;
+#ifndef TRIGPU_G_BITS_C
+#define TRIGPU_G_BITS_C 18
+#endif
+constexpr uint32_t kGBitsC = TRIGPU_G_BITS_C;  // coarse filter below the window: 2^18 bits (32 KB)
 constexpr size_t kGWinBytes = (size_t{1} << kGBitsA) / 8 + 16;
+constexpr size_t kGCoarseBytes = (size_t{1} << kGBitsC) / 8;
 
+// Below the window, a coarse shared-memory filter (bit i = some set element
+// in ranks [i << cs, (i + 1) << cs)) answers most probes; only its positives
+// read the exact global bitmap.
 struct WinGlobalProbe {
     static constexpr bool low = true;
     unsigned bm;          // shared address of the window
     uint32_t wb, la;      // window base, length
     const uint32_t* gbm;  // exact global bitmap of the set's elements below wb
+    unsigned bmc;         // shared address of the coarse filter
+    uint32_t cs;          // coarse shift
     __device__ __forceinline__ uint32_t bit(uint32_t y) const {
         const uint32_t o = min(y - wb, la);
         return (lds32(bit_word(bm, o)) >> (o & 31u)) & 1u;
     }
     __device__ __forceinline__ bool below(uint32_t y) const { return y < wb; }
-    __device__ __forceinline__ uint32_t cand(uint32_t y) const { return (__ldcg(gbm + (y >> 5)) >> (y & 31u)) & 1u; }
+    __device__ __forceinline__ uint32_t cand(uint32_t y) const {
+        const uint32_t c = y >> cs;
+        if (!((lds32(bit_word(bmc, c)) >> (c & 31u)) & 1u)) return 0u;
+        return (__ldcg(gbm + (y >> 5)) >> (y & 31u)) & 1u;
+    }
     __device__ __forceinline__ bool verify(uint32_t, bool act) const { return act; }
     __device__ __forceinline__ uint32_t sentinel() const { return kNone; }
 };
@@ -1159,7 +1249,8 @@ __global__ void __launch_bounds__(kGThreads) k_list_giant(ListParams P) {
     const unsigned warp = threadIdx.x >> 5;
     uint32_t* bm = P.bitmaps + (uint64_t)blockIdx.x * P.bitmap_words;
     uint32_t* win = reinterpret_cast<uint32_t*>(dsm + warp_scratch_bytes<F>(kGWarps));
-    constexpr uint32_t kWords = kGWinBytes / 4;
+    uint32_t* coarse = win + kGWinBytes / 4;
+    constexpr uint32_t kWords = (kGWinBytes + kGCoarseBytes) / 4;
     for (uint32_t i = threadIdx.x; i < kWords; i += kGThreads) win[i] = 0u;
     Sink<ALGO, F> sink;
     attach_scratch(sink, dsm);
@@ -1177,20 +1268,30 @@ __global__ void __launch_bounds__(kGThreads) k_list_giant(ListParams P) {
         const uint32_t la = 1u << (kGBitsA > P.bm_shrink + 5u ? kGBitsA - P.bm_shrink : 5u);
         const uint32_t s0 = __ldg(row), top = __ldg(row + d - 1);
         const uint32_t wb = top - s0 >= la ? top + 1u - la : s0;
+        // coarse shift: 2^kGBitsC bits cover the ranks below the window
+        const uint32_t cs = wb > (1u << kGBitsC) ? 32u - __clz((wb - 1u) >> kGBitsC) : 0u;
         for (uint32_t k = threadIdx.x; k < d; k += kGThreads) {
             const uint32_t v = __ldg(row + k);
-            if (v >= wb) atomicOr(win + ((v - wb) >> 5), 1u << ((v - wb) & 31u));
-            else atomicOr(bm + (v >> 5), 1u << (v & 31));
+            if (v >= wb) {
+                atomicOr(win + ((v - wb) >> 5), 1u << ((v - wb) & 31u));
+            } else {
+                atomicOr(bm + (v >> 5), 1u << (v & 31));
+                atomicOr(coarse + ((v >> cs) >> 5), 1u << ((v >> cs) & 31u));
+            }
         }
         __syncthreads();
-        const WinGlobalProbe probe{smem_addr(win), wb, la, bm};
+        const WinGlobalProbe probe{smem_addr(win), wb, la, bm, smem_addr(coarse), cs};
         scan_x_range<ALGO, F>(P, seed, so, warp * 32, d, kGWarps * 32, probe, sink);
         sink.end_unit(P, seed);
         __syncthreads();
         for (uint32_t k = threadIdx.x; k < d; k += kGThreads) {
             const uint32_t v = __ldg(row + k);
-            if (v >= wb) win[(v - wb) >> 5] = 0u;
-            else __stcg(bm + (v >> 5), 0u);
+            if (v >= wb) {
+                win[(v - wb) >> 5] = 0u;
+            } else {
+                __stcg(bm + (v >> 5), 0u);
+                coarse[(v >> cs) >> 5] = 0u;
+            }
         }
     }
     sink.flush(P);
@@ -1201,7 +1302,7 @@ __global__ void __launch_bounds__(kGThreads) k_list_giant(ListParams P) {
 template <unsigned F> constexpr size_t smem_reg() { return warp_scratch_bytes<F>(kRWarps) + kRWarps * kRBmBytes; }
 template <unsigned F> constexpr size_t smem_warp() { return warp_scratch_bytes<F>(kHWarps) + kHWarps * kHBmBytes; }
 template <unsigned F, class CFG> constexpr size_t smem_cta() { return warp_scratch_bytes<F>(CFG::kWarps) + cta_bitmap_bytes<CFG>() + cta_row_bytes<CFG>() + cta_ring_bytes<CFG>(); }
-template <unsigned F> constexpr size_t smem_giant() { return warp_scratch_bytes<F>(kGWarps) + kGWinBytes; }
+template <unsigned F> constexpr size_t smem_giant() { return warp_scratch_bytes<F>(kGWarps) + kGWinBytes + kGCoarseBytes; }
 
 // ---- seed classification --------------------------------------------------
 constexpr int kClasses = 5;  // R, H, C1, C2, G
@@ -1234,6 +1335,16 @@ __global__ void __launch_bounds__(256) k_classify_seeds(uint32_t rb, uint32_t re
             base = __shfl_sync(FULL, base, leader);
             if (cls == c) L.lists[c][base + __popc(b & lanemask_lt())] = (uint32_t)r;
         }
+    }
+}
+
+// List compaction: copy segment i's len triangles from src to dst (the
+// triangles past the count fill the chunk tails left below it).
+__global__ void k_move_triangles(const ulonglong2* __restrict__ seg_src_dst, const unsigned long long* __restrict__ seg_len,
+                                 unsigned nseg, uint32_t* __restrict__ tri) {
+    for (unsigned i = blockIdx.x; i < nseg; i += gridDim.x) {
+        const unsigned long long src = seg_src_dst[i].x, dst = seg_src_dst[i].y, len = seg_len[i];
+        for (unsigned long long k = threadIdx.x; k < 3 * len; k += blockDim.x) tri[3 * dst + k] = tri[3 * src + k];
     }
 }
 

@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <vector>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -111,6 +112,7 @@ struct tl_ctx {
     unsigned long long cost[4] = {0, 0, 0, 0};
     double h2d_ms = 0, orient_ms = 0;
 
+    DevBuf holes, segs;  // list compaction: chunk tails {start, len}; move segments
     DevBuf goff, gadj, rank, inv, hv, sort_tmp, labels, radj, out_off, out_adj, in_off, in_adj, outdeg, indeg, lists, acc,
         vcount, tri, scan_part, bitmaps, small;
     bool have_vcounts = false, have_tri = false;
@@ -649,7 +651,7 @@ TL_API void tl_destroy(tl_ctx* ctx) {
     DevBuf* bufs[] = {&ctx->goff,   &ctx->gadj,   &ctx->rank,  &ctx->inv,    &ctx->radj,      &ctx->out_off,
                       &ctx->out_adj, &ctx->in_off, &ctx->in_adj, &ctx->outdeg, &ctx->indeg,     &ctx->lists,
                       &ctx->acc,    &ctx->vcount, &ctx->tri,   &ctx->scan_part, &ctx->bitmaps, &ctx->small,
-                      &ctx->hv,     &ctx->sort_tmp, &ctx->labels};
+                      &ctx->hv,     &ctx->sort_tmp, &ctx->labels, &ctx->holes, &ctx->segs};
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     for (auto& ev : ctx->ev) cudaEventDestroy(ev);
@@ -1056,19 +1058,20 @@ TL_API tl_status tl_list_range(tl_ctx* ctx, int algo, unsigned out_flags, uint32
     CK(cudaEventRecord(ctx->ev[PH_COUNT + 4], ctx->s));  // listing kernels start
     auto run = [&](unsigned F) -> tl_status {
         for (bool& r : ctx->cls_run) r = false;
-        CK(cudaMemsetAsync(acc, 0, 8 * sizeof(unsigned long long), ctx->s));
+        CK(cudaMemsetAsync(acc, 0, 8 * sizeof(unsigned long long), ctx->s));  // counts, checksum, list cursors
         CK(cudaMemsetAsync(counts + 8, 0, 8 * sizeof(unsigned int), ctx->s));
         if (F & F_VCOUNT) CK(cudaMemsetAsync(ctx->vcount.p, 0, (size_t)n * 8, ctx->s));
         return algo == TL_ALGO_APM ? launch_flags<ALGO_APM>(ctx, F, base, lists, h, counts + 8)
                                    : launch_flags<ALGO_APP>(ctx, F, base, lists, h, counts + 8);
     };
-    unsigned long long res[3] = {0, 0, 0};
+    unsigned long long res[4] = {0, 0, 0, 0};
+    constexpr unsigned kHolesCap = 1u << 17;  // >= every warp of every class launch
     if (want_list) {
         // One pass into the context's triangle buffer (grow-only, kept across
-        // calls): the cursor counts every triangle, writes stop at capacity.
-        // Only when the list outgrows the buffer is it grown to the exact
-        // size and the pass repeated. First call: a quarter of the free
-        // device memory, at most 2^31 triangles.
+        // calls): warps claim kListChunk slots at a time, writes stop at
+        // capacity. Only when the claims outgrow the buffer is it grown and
+        // the pass repeated. First call: a quarter of the free device memory,
+        // at most 2^31 triangles.
         if (ctx->tri.cap < 12 * 64) {
             size_t free_b = 0, total_b = 0;
             if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
@@ -1078,21 +1081,87 @@ TL_API tl_status tl_list_range(tl_ctx* ctx, int algo, unsigned out_flags, uint32
             const size_t want = std::min<size_t>(free_b / 4, (size_t{1} << 31) * 12);
             ENSURE(tri, std::max<size_t>(want / 12 * 12, 12 * 64));
         }
+        ENSURE(holes, (size_t)kHolesCap * 16);
         base.tri = P<uint32_t>(ctx->tri);
         base.tri_cap = ctx->tri.cap / 12;
+        base.holes = P<ulonglong2>(ctx->holes);
+        base.holes_cap = kHolesCap;
     }
     st = run(out_flags);
     if (st != TL_OK) return st;
     CK(cudaMemcpyAsync(res, acc, sizeof(res), cudaMemcpyDeviceToHost, ctx->s));
     CK(cudaStreamSynchronize(ctx->s));
     if (want_list && res[2] > base.tri_cap) {
-        ENSURE(tri, (size_t)res[2] * 12);
+        ENSURE(tri, (size_t)res[2] * 12 + (size_t)kListChunk * 12 * 4096);
         base.tri = P<uint32_t>(ctx->tri);
         base.tri_cap = ctx->tri.cap / 12;
         st = run(out_flags);
         if (st != TL_OK) return st;
         CK(cudaMemcpyAsync(res, acc, sizeof(res), cudaMemcpyDeviceToHost, ctx->s));
         CK(cudaStreamSynchronize(ctx->s));
+        if (res[2] > base.tri_cap)
+            return ctx->fail(TL_ERR_CUDA, "tl_list: list claims outgrew the regrown buffer");
+    }
+    if (want_list) {
+        // Compaction: the chunks hold every triangle in [0, claimed) except
+        // the recorded tails; move the triangles above the count into the
+        // tails below it (at most one tail per warp).
+        const unsigned long long T = res[0], claimed = res[2], nh = res[3];
+        if (nh > kHolesCap) return ctx->fail(TL_ERR_CUDA, "tl_list: too many list chunk tails");
+        std::vector<std::pair<unsigned long long, unsigned long long>> hs(nh);
+        if (nh) {
+            std::vector<ulonglong2> hv(nh);
+            CK(cudaMemcpyAsync(hv.data(), ctx->holes.p, nh * 16, cudaMemcpyDeviceToHost, ctx->s));
+            CK(cudaStreamSynchronize(ctx->s));
+            for (size_t i = 0; i < nh; ++i) hs[i] = {hv[i].x, hv[i].y};
+            std::sort(hs.begin(), hs.end());
+        }
+        unsigned long long hole_total = 0;
+        for (auto& h : hs) hole_total += h.second;
+        if (claimed - hole_total != T)
+            return ctx->fail(TL_ERR_CUDA, "tl_list: list slots disagree with the triangle count");
+        // destinations: tail parts below T; sources: the filled ranges in [T, claimed)
+        std::vector<std::pair<unsigned long long, unsigned long long>> dst, src;
+        unsigned long long pos = T;
+        for (auto& h : hs) {
+            if (h.first < T) dst.push_back({h.first, std::min(h.first + h.second, T) - h.first});
+            const unsigned long long hb = std::max(h.first, T), he = h.first + h.second;
+            if (he > T) {
+                if (hb > pos) src.push_back({pos, hb - pos});
+                pos = std::max(pos, he);
+            }
+        }
+        if (claimed > pos) src.push_back({pos, claimed - pos});
+        std::vector<ulonglong2> seg;
+        std::vector<unsigned long long> seglen;
+        size_t si = 0;
+        unsigned long long soff = 0;
+        for (auto& d : dst) {
+            unsigned long long doff = 0;
+            while (doff < d.second) {
+                if (si >= src.size()) return ctx->fail(TL_ERR_CUDA, "tl_list: list compaction ran out of sources");
+                const unsigned long long len = std::min(d.second - doff, src[si].second - soff);
+                seg.push_back(make_ulonglong2(src[si].first + soff, d.first + doff));
+                seglen.push_back(len);
+                doff += len;
+                soff += len;
+                if (soff == src[si].second) {
+                    ++si;
+                    soff = 0;
+                }
+            }
+        }
+        if (!seg.empty()) {
+            ENSURE(segs, seg.size() * 24);
+            auto* d_seg = P<ulonglong2>(ctx->segs);
+            auto* d_len = reinterpret_cast<unsigned long long*>(d_seg + seg.size());
+            CK(cudaMemcpyAsync(d_seg, seg.data(), seg.size() * 16, cudaMemcpyHostToDevice, ctx->s));
+            CK(cudaMemcpyAsync(d_len, seglen.data(), seg.size() * 8, cudaMemcpyHostToDevice, ctx->s));
+            k_move_triangles<<<grid_for(seg.size(), 1, ctx->sms * 8), 256, 0, ctx->s>>>(d_seg, d_len, (unsigned)seg.size(),
+                                                                                        P<uint32_t>(ctx->tri));
+            LAUNCHED();
+        }
+        res[2] = T;
     }
     CK(cudaEventRecord(ctx->ev[PH_LIST], ctx->s));
     CK(cudaEventSynchronize(ctx->ev[PH_LIST]));
