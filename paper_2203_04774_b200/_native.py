@@ -194,6 +194,10 @@ def trihost() -> C.CDLL:
     lib.th_graph_to_csr.restype = C.c_int
     lib.th_graph_labels.argtypes = [_vp, _vp]
     lib.th_graph_labels.restype = None
+    lib.th_parse_edgelist.argtypes = [C.c_char_p, C.POINTER(C.POINTER(C.c_int64)), C.POINTER(_u64)]
+    lib.th_parse_edgelist.restype = C.c_int
+    lib.th_free.argtypes = [_vp]
+    lib.th_free.restype = None
     lib.th_order.argtypes = [_vp, C.c_char_p, _u64, _vp, C.POINTER(C.c_double)]
     lib.th_order.restype = C.c_int
     lib.th_cost.argtypes = [_vp, _vp, _vp]

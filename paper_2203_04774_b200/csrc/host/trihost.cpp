@@ -8,7 +8,14 @@
 
 #include "trihost.h"
 
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
 #include <algorithm>
+#include <charconv>
+#include <cstdint>
 #include <atomic>
 #include <chrono>
 #include <cmath>
@@ -428,6 +435,139 @@ void* th_graph_load(const char* path, std::uint64_t* loops, std::uint64_t* dups)
         return nullptr;
     }
 }
+
+// Native edge-list reader: the same line grammar as the reference's
+// load_edgelist (graph.cpp:164-186) -- getline lines, one trailing '\r'
+// dropped, tokens split on ' ' / '\t', empty lines and lines whose first token
+// starts with '#' skipped, two std::from_chars int64 labels and nothing after
+// them, else "line N: ..." (ParseError, common.hpp:16-20) for the FIRST bad
+// line -- over an mmap of the file, one contiguous slice of lines per thread,
+// slices concatenated in file order. The raw pairs (loops and duplicates
+// kept) are what normalize() takes (graph.cpp:115), so the GPU normalize
+// (tl_normalize) finishes the reference's load_edgelist_file.
+int th_parse_edgelist(const char* path, std::int64_t** edges, std::uint64_t* k) {
+    *edges = nullptr;
+    *k = 0;
+    const int fd = ::open(path, O_RDONLY);
+    if (fd < 0) {
+        g_err = std::string("cannot open edge list: ") + path;
+        return -1;
+    }
+    struct stat sb {};
+    if (::fstat(fd, &sb) != 0) {
+        ::close(fd);
+        g_err = std::string("cannot stat edge list: ") + path;
+        return -1;
+    }
+    const std::size_t size = static_cast<std::size_t>(sb.st_size);
+    const char* data = nullptr;
+    if (size) {
+        void* p = ::mmap(nullptr, size, PROT_READ, MAP_PRIVATE, fd, 0);
+        if (p == MAP_FAILED) {
+            ::close(fd);
+            g_err = std::string("cannot map edge list: ") + path;
+            return -1;
+        }
+        data = static_cast<const char*>(p);
+    }
+    ::close(fd);
+    const unsigned T = static_cast<unsigned>(std::max<std::size_t>(1, std::min<std::size_t>(nthreads(), size / (1u << 20) + 1)));
+    // slice t = the lines STARTING in [cut[t], cut[t+1])
+    std::vector<std::size_t> cut(T + 1, size);
+    cut[0] = 0;
+    for (unsigned t = 1; t < T; ++t) {
+        std::size_t c = size * t / T;
+        const void* nl = c < size ? std::memchr(data + c, '\n', size - c) : nullptr;
+        cut[t] = nl ? static_cast<std::size_t>(static_cast<const char*>(nl) - data) + 1 : size;
+        cut[t] = std::max(cut[t], cut[t - 1]);
+    }
+    struct Slice {
+        std::vector<std::int64_t> e;
+        std::size_t bad = SIZE_MAX;  // byte offset of the first bad line
+        std::string what;
+    };
+    std::vector<Slice> sl(T);
+    auto is_sep = [](char c) { return c == ' ' || c == '\t'; };
+    auto parse = [&](unsigned t) {
+        Slice& s = sl[t];
+        s.e.reserve((cut[t + 1] - cut[t]) / 8);
+        std::size_t pos = cut[t];
+        const std::size_t end = cut[t + 1];
+        while (pos < end) {
+            const char* nl = static_cast<const char*>(std::memchr(data + pos, '\n', size - pos));
+            const std::size_t le = nl ? static_cast<std::size_t>(nl - data) : size;  // line [pos, le)
+            std::size_t lend = le;
+            if (lend > pos && data[lend - 1] == '\r') --lend;
+            std::size_t i = pos;
+            auto token = [&](std::size_t& b, std::size_t& e) {
+                while (i < lend && is_sep(data[i])) ++i;
+                b = i;
+                while (i < lend && !is_sep(data[i])) ++i;
+                e = i;
+            };
+            std::size_t ub, ue, vb, ve, tb, te;
+            token(ub, ue);
+            if (ue > ub && data[ub] != '#') {
+                token(vb, ve);
+                std::int64_t u = 0, v = 0;
+                auto ok = [&](std::size_t b, std::size_t e, std::int64_t& out) {
+                    const auto r = std::from_chars(data + b, data + e, out);
+                    return r.ec == std::errc{} && r.ptr == data + e;
+                };
+                if (ve == vb || !ok(ub, ue, u) || !ok(vb, ve, v)) {
+                    s.bad = pos;
+                    s.what = "expected two integer labels, got \"" + std::string(data + pos, lend - pos) + "\"";
+                    return;
+                }
+                token(tb, te);
+                if (te > tb) {
+                    s.bad = pos;
+                    s.what = "trailing tokens after edge pair";
+                    return;
+                }
+                s.e.push_back(u);
+                s.e.push_back(v);
+            }
+            pos = le + 1;
+        }
+    };
+    if (T == 1) {
+        parse(0);
+    } else {
+        std::vector<std::thread> pool;
+        for (unsigned t = 0; t < T; ++t) pool.emplace_back(parse, t);
+        for (auto& th : pool) th.join();
+    }
+    int rc = 0;
+    std::uint64_t total = 0;
+    for (unsigned t = 0; t < T && rc == 0; ++t) {
+        if (sl[t].bad != SIZE_MAX) {  // the first bad line in file order
+            const std::size_t line = 1 + static_cast<std::size_t>(std::count(data, data + sl[t].bad, '\n'));
+            g_err = "line " + std::to_string(line) + ": " + sl[t].what;
+            rc = -1;
+        }
+        total += sl[t].e.size();
+    }
+    if (rc == 0 && total) {
+        auto* out = static_cast<std::int64_t*>(std::malloc(total * sizeof(std::int64_t)));
+        if (!out) {
+            g_err = "edge list: out of host memory";
+            rc = -1;
+        } else {
+            std::uint64_t o = 0;
+            for (auto& s : sl) {
+                std::copy(s.e.begin(), s.e.end(), out + o);
+                o += s.e.size();
+            }
+            *edges = out;
+            *k = total / 2;
+        }
+    }
+    if (data) ::munmap(const_cast<char*>(data), size);
+    return rc;
+}
+
+void th_free(void* p) { std::free(p); }
 
 int th_graph_to_csr(void* graph, th_csr* out) {
     return csr_from_graph(*static_cast<trilist::Graph*>(graph), out);

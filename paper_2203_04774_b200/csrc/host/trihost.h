@@ -49,11 +49,19 @@ int th_csr_check(const th_csr* g);
 void* th_graph_new(const th_csr* g);
 void th_graph_free(void* graph);
 /* The reference's text loader (load_edgelist_file, graph.cpp:164-192: one
- * "a b" label pair per line, '#' / '%' comments, normalize()). The handle
+ * "a b" label pair per line, lines whose first token starts with '#' skipped,
+ * normalize()). The handle
  * works with th_order / th_cost; th_graph_to_csr copies its CSR out,
  * th_graph_labels its labels (int64[n], dense id -> original label). */
 void* th_graph_load(const char* path, uint64_t* loops_removed, uint64_t* duplicates_removed);
 int th_graph_to_csr(void* graph, th_csr* out);
+/* Native multi-threaded reader of the same text format (mmap, one slice of
+ * lines per thread; grammar and "line N: ..." errors of load_edgelist,
+ * graph.cpp:164-186): *edges = k raw (a, b) int64 label pairs in file order,
+ * loops and duplicates kept (normalize's input, graph.cpp:115); free with
+ * th_free. Feed them to tl_normalize. 0 ok, -1 error (th_last_error). */
+int th_parse_edgelist(const char* path, int64_t** edges, uint64_t* k);
+void th_free(void* p);
 void th_graph_labels(void* graph, int64_t* out);
 /* Ordering by reference method name: identity random degree core split check
  * neigh (trilist_cli.cpp:47-64). rank_out[v] = 0-based position of v. */

@@ -280,6 +280,25 @@ def gen_ws(n: int, k: int = 32, p: float = 0.1, seed: int = 1) -> Graph:
     return _gen(_native.trihost().th_gen_ws, n, k, p, seed)
 
 
+def parse_edgelist(path: str) -> np.ndarray:
+    """Raw (k, 2) int64 label pairs of a text edge list, in file order, loops and
+    duplicates kept: the native multi-threaded reader (th_parse_edgelist) of
+    load_edgelist's grammar (graph.cpp:164-186; errors "line N: ..." as its
+    ParseError). The input of normalize (graph.cpp:115) -- Context.normalize
+    runs that on the GPU."""
+    lib = _native.trihost()
+    ptr = C.POINTER(C.c_int64)()
+    k = C.c_uint64(0)
+    if lib.th_parse_edgelist(path.encode(), C.byref(ptr), C.byref(k)) != 0:
+        raise HostError(_th_err())
+    if k.value == 0:
+        return np.zeros((0, 2), np.int64)
+    try:
+        return np.ctypeslib.as_array(ptr, shape=(k.value, 2)).copy()
+    finally:
+        lib.th_free(ptr)
+
+
 def host_threads() -> int:
     return int(_native.trihost().th_threads())
 

@@ -97,3 +97,65 @@ def test_unknown_ordering_raises():
     g = tg.gen_gnm(10, 10, 1)
     with pytest.raises(host.HostError):
         host.compute_order(g, "bogus")
+
+
+def _write(tmp_path, name, text):
+    p = tmp_path / name
+    p.write_bytes(text.encode() if isinstance(text, str) else text)
+    return str(p)
+
+
+def test_parse_edgelist_matches_reference_loader(tmp_path):
+    """The native reader (th_parse_edgelist) + the reference's normalize equals
+    the reference's own load_edgelist_file (graph.cpp:164-192): same n, m,
+    loop / duplicate counts, CSR and labels, on the grammar's corner cases
+    (CRLF, tabs, blank and '#' lines, negative and extreme labels, no final
+    newline) and on a large multi-slice file."""
+    import oracle
+    rng = np.random.default_rng(5)
+    cases = {
+        "toy": "0 1\n0 2\n1 2\n2 3\n",  # cli_test.cpp's toy graph
+        "crlf": "# header\r\n10\t-3\r\n\r\n-3 10\r\n  7   7  \r\n7 10",
+        "extreme": f"{-2**63} {2**63 - 1}\n#c\n\t\n5 {-2**63}\n",
+        "empty": "",
+        "comments": "# only\n#\n",
+    }
+    lines = [f"{a} {b}" for a, b in rng.integers(-10**12, 10**12, size=(120_000, 2))]
+    lines[::7] = [f"{a}\t{a}" for a in rng.integers(0, 50, size=len(lines[::7]))]
+    cases["big"] = "\n".join(lines) + "\n"
+    for name, text in cases.items():
+        p = _write(tmp_path, name + ".txt", text)
+        raw = tg.host.parse_edgelist(p)
+        ref = tg.Graph.load(p)
+        if raw.shape[0] == 0:
+            assert ref.n == 0 and ref.m == 0
+            continue
+        rg, lo, du = oracle.RefGraph.normalize(raw)
+        off, adj = rg.csr()
+        assert (rg.n, rg.m, lo, du) == (ref.n, ref.m, ref.loops_removed, ref.duplicates_removed), name
+        assert np.array_equal(off, ref.offsets) and np.array_equal(adj, ref.adjacency), name
+        assert np.array_equal(rg.labels(), ref.labels), name
+
+
+def test_parse_edgelist_errors_match_reference(tmp_path):
+    """Bad lines raise the reference's ParseError text ("line N: ...",
+    common.hpp:16-20, graph.cpp:180-183) for the FIRST bad line, also when
+    it sits deep in a multi-slice file."""
+    good = "\n".join(f"{i} {i + 1}" for i in range(300_000))
+    for name, text in {
+        "one_token": "1 2\n3\n",
+        "trailing": "1 2\n3 4 5\n",
+        "plus": "1 2\n+3 4\n",
+        "word": "1 2\nx 4\n",
+        "overflow": f"1 {2**63}\n",
+        "deep": good + "\n1 2 3\n" + good + "\nbad\n",
+        "percent": "% comment\n1 2\n",
+    }.items():
+        p = _write(tmp_path, name + ".txt", text)
+        with pytest.raises(tg.host.HostError) as ours:
+            tg.host.parse_edgelist(p)
+        with pytest.raises(tg.host.HostError) as theirs:
+            tg.Graph.load(p)
+        assert str(ours.value) == str(theirs.value), name
+    with pytest.raises(tg.host.HostError, match="cannot open"):
+        tg.host.parse_edgelist(str(tmp_path / "missing.txt"))
