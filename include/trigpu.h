@@ -116,7 +116,10 @@ TL_API tl_status tl_fetch_ranks(tl_ctx* ctx, uint32_t* rank);
  * dense id = label rank) + Graph::from_dense_edges (graph.cpp:13-56: sorted
  * rows). edges = k (a, b) int64 label pairs (host). The graph stays on the
  * device: tl_fetch_graph copies out offsets (n+1), adj (2m) and labels (n);
- * tl_orient_normalized orients it with a device ordering (TL_ORDER_*). */
+ * tl_orient_normalized orients it with a device ordering (TL_ORDER_*).
+ * 64-bit item counts (k up to 2^40, memory permitting: 48 bytes of device
+ * scratch per raw edge); more than 2^32 - 2^20 distinct labels is
+ * TL_ERR_INVALID_ARGUMENT. Text files: th_parse_edgelist (trihost.h). */
 TL_API tl_status tl_normalize(tl_ctx* ctx, uint64_t k, const int64_t* edges, uint32_t* n, uint64_t* m,
                               uint64_t* loops_removed, uint64_t* duplicates_removed);
 TL_API tl_status tl_fetch_graph(tl_ctx* ctx, uint64_t* offsets, uint32_t* adj, int64_t* labels);

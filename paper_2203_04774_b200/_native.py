@@ -174,6 +174,8 @@ def trihost() -> C.CDLL:
     P = C.POINTER(ThCsr)
     lib.th_gen_gnm.argtypes = [_u32, _u64, _u64, P]
     lib.th_gen_rmat.argtypes = [_u32, _u32, _u64, P]
+    lib.th_gen_rmat_raw.argtypes = [_u32, _u32, _u64, _vp]
+    lib.th_gen_rmat_raw.restype = C.c_int
     lib.th_gen_chung_lu.argtypes = [_u32, _u64, C.c_double, C.c_double, C.c_double, _u64, P]
     lib.th_gen_ws.argtypes = [_u32, _u32, C.c_double, _u64, P]
     lib.th_csr_from_pairs.argtypes = [_u32, _u64, _vp, P]

@@ -224,44 +224,70 @@ int th_gen_gnm(std::uint32_t n, std::uint64_t m, std::uint64_t seed, th_csr* out
 // R-MAT (a,b,c,d) = (0.57, 0.19, 0.19, 0.05); per level one 32-bit half of a
 // draw against integer thresholds round(x * 2^32). Draw i uses stream 1,
 // indices i*ceil(scale/2) ... Symmetrised, deduplicated, loops dropped.
+namespace {
+// Draw i of the R-MAT recipe: `scale` quadrant picks, two per 64-bit draw.
+struct RmatDraw {
+    static constexpr std::uint32_t tA = 2448131359u;    // round(0.57 * 2^32)
+    static constexpr std::uint32_t tAB = 3264175145u;   // round(0.76 * 2^32)
+    static constexpr std::uint32_t tABC = 4080218931u;  // round(0.95 * 2^32)
+    std::uint32_t scale, per;
+    Stream rng;
+    RmatDraw(std::uint32_t scale_, std::uint64_t seed) : scale(scale_), per((scale_ + 1) / 2), rng(seed, 1) {}
+    void operator()(std::uint64_t i, std::uint32_t& u, std::uint32_t& v) const {
+        u = 0;
+        v = 0;
+        for (std::uint32_t l = 0; l < scale; ++l) {
+            const std::uint64_t r64 = rng(i * per + l / 2);
+            const std::uint32_t r = (l & 1) ? static_cast<std::uint32_t>(r64) : static_cast<std::uint32_t>(r64 >> 32);
+            const std::uint32_t bu = r >= tAB, bv = (r >= tA && r < tAB) || r >= tABC;
+            u = (u << 1) | bu;
+            v = (v << 1) | bv;
+        }
+    }
+};
+}  // namespace
+
 int th_gen_rmat(std::uint32_t scale, std::uint32_t edge_factor, std::uint64_t seed, th_csr* out) {
     if (scale < 1 || scale > 31) {
         g_err = "rmat: scale must be in [1, 31]";
         return -1;
     }
-    constexpr std::uint32_t tA = 2448131359u;    // round(0.57 * 2^32)
-    constexpr std::uint32_t tAB = 3264175145u;   // round(0.76 * 2^32)
-    constexpr std::uint32_t tABC = 4080218931u;  // round(0.95 * 2^32)
     const std::uint32_t n = 1u << scale;
     const std::uint64_t draws = static_cast<std::uint64_t>(edge_factor) << scale;
-    const std::uint32_t per = (scale + 1) / 2;
-    const Stream rng(seed, 1);
+    const RmatDraw draw(scale, seed);
     std::vector<std::uint64_t> keys(2 * draws);
-    std::atomic<std::uint64_t> loops{0};
     parallel_for(draws, [&](unsigned, std::uint64_t b, std::uint64_t e) {
-        std::uint64_t lp = 0;
         for (std::uint64_t i = b; i < e; ++i) {
-            std::uint32_t u = 0, v = 0;
-            for (std::uint32_t l = 0; l < scale; ++l) {
-                const std::uint64_t r64 = rng(i * per + l / 2);
-                const std::uint32_t r = (l & 1) ? static_cast<std::uint32_t>(r64) : static_cast<std::uint32_t>(r64 >> 32);
-                const std::uint32_t bu = r >= tAB, bv = (r >= tA && r < tAB) || r >= tABC;
-                u = (u << 1) | bu;
-                v = (v << 1) | bv;
-            }
+            std::uint32_t u, v;
+            draw(i, u, v);
             if (u == v) {
                 keys[2 * i] = keys[2 * i + 1] = ~0ULL;
-                ++lp;
             } else {
                 keys[2 * i] = (static_cast<std::uint64_t>(u) << 32) | v;
                 keys[2 * i + 1] = (static_cast<std::uint64_t>(v) << 32) | u;
             }
         }
-        loops += lp;
     });
-    // drop loop markers (they sort last once the radix covers the key bits,
-    // but ~0 is outside the sorted bit range, so filter explicitly)
+    // loop markers (~0) are dropped by csr_from_keys
     return csr_from_keys(n, keys, out);
+}
+
+int th_gen_rmat_raw(std::uint32_t scale, std::uint32_t edge_factor, std::uint64_t seed, std::int64_t* out) {
+    if (scale < 1 || scale > 31) {
+        g_err = "rmat: scale must be in [1, 31]";
+        return -1;
+    }
+    const std::uint64_t draws = static_cast<std::uint64_t>(edge_factor) << scale;
+    const RmatDraw draw(scale, seed);
+    parallel_for(draws, [&](unsigned, std::uint64_t b, std::uint64_t e) {
+        for (std::uint64_t i = b; i < e; ++i) {
+            std::uint32_t u, v;
+            draw(i, u, v);
+            out[2 * i] = u;
+            out[2 * i + 1] = v;
+        }
+    });
+    return 0;
 }
 
 // Chung-Lu: w_i = min(wmin * (1-U)^(-1/(exponent-1)), wmax) (Pareto tail

@@ -35,6 +35,9 @@ int th_threads(void);
 /* Generators. Each returns 0 and fills *out (free with th_csr_free). */
 int th_gen_gnm(uint32_t n, uint64_t m, uint64_t seed, th_csr* out);
 int th_gen_rmat(uint32_t scale, uint32_t edge_factor, uint64_t seed, th_csr* out);
+/* The raw draws of th_gen_rmat (edge_factor << scale (u, v) pairs as int64,
+ * loops and duplicates kept): normalize's input for the same graph. */
+int th_gen_rmat_raw(uint32_t scale, uint32_t edge_factor, uint64_t seed, int64_t* out);
 int th_gen_chung_lu(uint32_t n, uint64_t draws, double exponent, double wmin, double wmax,
                     uint64_t seed, th_csr* out);
 int th_gen_ws(uint32_t n, uint32_t k, double p, uint64_t seed, th_csr* out);

@@ -8,76 +8,74 @@
 //   * labels = the sorted distinct endpoint labels; dense id = rank of the
 //     label (lower_bound);
 //   * CSR rows = the sorted neighbour lists (uint64 offsets, uint32 ids).
-// Device plan: canonicalise (loops -> a sentinel pair that sorts last), sort
-// the pairs by (a, b) with two stable LSD radix sorts, flag first-of-run,
-// compact; labels by radix sort + unique over the 2m endpoints; dense ids by
-// binary search; the 2m directed pairs as 64-bit keys (src << 32 | dst), one
-// radix sort gives the rows already sorted; offsets from a degree count + scan.
+// Device plan (64-bit item counts throughout; 48 bytes of scratch per raw edge):
+//   1. endpoints of the non-loop edges (flags + DeviceSelect::Flagged), radix
+//      sort, unique -> labels (the dedup cannot remove a label: duplicates
+//      share endpoints, so this is the label set of the kept edges);
+//   2. each raw edge -> one 64-bit key (min dense id << 32 | max dense id) by
+//      binary search in the labels (the label -> id map is monotone, so the
+//      min label gives the min id); loops -> ~0, which sorts last;
+//   3. radix sort + unique of the keys: the kept edges in (a, b) order, i.e.
+//      normalize's sorted, deduplicated edge list; the loop key is dropped;
+//   4. both directions as (src << 32 | dst) keys, one radix sort gives the
+//      sorted rows; offsets from degree counts + scan (from_dense_edges).
 #pragma once
 
 #include "common.cuh"
 
 namespace trigpu {
 
-constexpr long long kLoopSentinel = 0x7FFFFFFFFFFFFFFFll;
+constexpr unsigned long long kLoopKey = ~0ull;
 
-__global__ void k_canon_edges(uint64_t k, const long long* __restrict__ raw, long long* __restrict__ a,
-                              long long* __restrict__ b, unsigned long long* loops) {
+// flags[2i] = flags[2i + 1] = edge i is not a loop
+__global__ void k_loop_flags(uint64_t k, const long long* __restrict__ raw, unsigned char* __restrict__ flags,
+                             unsigned long long* loops) {
     unsigned long long lc = 0;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < k; i += stride) {
-        const long long x = raw[2 * i], y = raw[2 * i + 1];
-        if (x == y) {
-            a[i] = kLoopSentinel;
-            b[i] = kLoopSentinel;
-            ++lc;
-        } else {
-            a[i] = x < y ? x : y;
-            b[i] = x < y ? y : x;
-        }
+        const bool keep = raw[2 * i] != raw[2 * i + 1];
+        flags[2 * i] = keep;
+        flags[2 * i + 1] = keep;
+        lc += !keep;
     }
     lc = warp_sum64(lc);
     if (lane_id() == 0 && lc) atomicAdd(loops, lc);
 }
 
-// keep[i] = first of its (a, b) run and not a loop (pairs sorted by (a, b))
-__global__ void k_first_of_run(uint64_t k, const long long* __restrict__ a, const long long* __restrict__ b,
-                               unsigned char* __restrict__ keep) {
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < k; i += stride) {
-        const bool loop = a[i] == kLoopSentinel;
-        keep[i] = !loop && (i == 0 || a[i] != a[i - 1] || b[i] != b[i - 1]);
-    }
-}
-
-__global__ void k_interleave_endpoints(uint64_t m, const long long* __restrict__ a, const long long* __restrict__ b,
-                                       long long* __restrict__ ends) {
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += stride) {
-        ends[2 * i] = a[i];
-        ends[2 * i + 1] = b[i];
-    }
-}
-
 __device__ __forceinline__ uint32_t label_rank(const long long* __restrict__ labels, uint32_t n, long long x) {
     uint32_t lo = 0, hi = n;
     while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
+        const uint32_t mid = lo + ((hi - lo) >> 1);
         if (labels[mid] < x) lo = mid + 1;
         else hi = mid;
     }
     return lo;
 }
 
-// Directed pair keys (src << 32 | dst) for both directions of every edge,
-// and the degree counts.
-__global__ void k_dense_keys(uint64_t m, const long long* __restrict__ a, const long long* __restrict__ b,
-                             const long long* __restrict__ labels, uint32_t n,
-                             unsigned long long* __restrict__ keys, uint32_t* __restrict__ deg) {
+// One undirected key per raw edge: (min id << 32 | max id), loops -> kLoopKey.
+__global__ void k_edge_keys(uint64_t k, const long long* __restrict__ raw, const long long* __restrict__ labels,
+                            uint32_t n, unsigned long long* __restrict__ keys) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < k; i += stride) {
+        const long long x = raw[2 * i], y = raw[2 * i + 1];
+        if (x == y) {
+            keys[i] = kLoopKey;
+            continue;
+        }
+        const uint32_t u = label_rank(labels, n, x < y ? x : y), v = label_rank(labels, n, x < y ? y : x);
+        keys[i] = (static_cast<unsigned long long>(u) << 32) | v;
+    }
+}
+
+// Directed pair keys (src << 32 | dst) for both directions of the m kept
+// edges, and the degree counts.
+__global__ void k_directed_keys(uint64_t m, const unsigned long long* __restrict__ edges,
+                                unsigned long long* __restrict__ keys, uint32_t* __restrict__ deg) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += stride) {
-        const uint32_t u = label_rank(labels, n, a[i]), v = label_rank(labels, n, b[i]);
-        keys[2 * i] = (static_cast<unsigned long long>(u) << 32) | v;
+        const unsigned long long e = edges[i];
+        const uint32_t u = static_cast<uint32_t>(e >> 32), v = static_cast<uint32_t>(e);
+        keys[2 * i] = e;
         keys[2 * i + 1] = (static_cast<unsigned long long>(v) << 32) | u;
         atomicAdd(&deg[u], 1u);
         atomicAdd(&deg[v], 1u);

@@ -790,101 +790,106 @@ TL_API tl_status tl_normalize(tl_ctx* ctx, uint64_t k, const int64_t* edges, uin
     ctx->normalized = false;
     ctx->oriented = false;  // goff / gadj / outdeg / radj are reused below
     drop_results(ctx);
-    if (k >= (1ull << 30)) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "normalize: more than 2^30 - 1 raw edges");
-    // scratch: raw (2k) | a, b (k each) | a2, b2 (k each) in radj-sized buffers
-    ENSURE(radj, std::max<size_t>(k * 16 * 3 + 64, 64));
+    if (k > (1ull << 40)) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "normalize: more than 2^40 raw edges");
+    // scratch: three regions of 16k bytes in radj (see normalize.cuh)
+    const size_t R = std::max<size_t>(k * 16, 64);
+    ENSURE(radj, 3 * R);
     ENSURE(small, 128);
-    auto* flags = static_cast<unsigned long long*>(ctx->small.p);
+    auto* flags = static_cast<unsigned long long*>(ctx->small.p);  // [0] loops, [2] / [3] selected counts
     CK(cudaMemsetAsync(flags, 0, 64, ctx->s));
-    long long* raw = P<long long>(ctx->radj);
-    long long* a = raw + 2 * k;
-    long long* b = a + k;
-    long long* a2 = b + k;
-    long long* b2 = a2 + k;
+    auto* base = static_cast<unsigned char*>(ctx->radj.p);
+    long long* raw = reinterpret_cast<long long*>(base);
+    unsigned char* r1 = base + R;
+    unsigned char* r2 = base + 2 * R;
+    auto* nsel = reinterpret_cast<long long*>(flags + 2);
+    const unsigned big = ctx->sms * 16;
     if (k) CK(cudaMemcpyAsync(raw, edges, k * 16, cudaMemcpyHostToDevice, ctx->s));
-    const unsigned grid = grid_for(std::max<uint64_t>(k, 1), 256, ctx->sms * 16);
-    if (k) {
-        k_canon_edges<<<grid, 256, 0, ctx->s>>>(k, raw, a, b, flags);
-        LAUNCHED();
-    }
-    // sort by (a, b): stable LSD, first by b then by a; raw's space is free now
-    size_t tb = 0, tmp_bytes = 0;
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, b, b2, a, a2, (int)k, 0, 64, ctx->s));
+    // cub scratch for the largest call of each kind
+    size_t tmp_bytes = 0, tb = 0;
+    const int64_t k2 = static_cast<int64_t>(2 * k);
+    CK(cub::DeviceSelect::Flagged(nullptr, tb, raw, r2, reinterpret_cast<long long*>(r1), nsel, k2, ctx->s));
     tmp_bytes = std::max(tmp_bytes, tb);
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, a2, a, b2, b, (int)k, 0, 64, ctx->s));
+    CK(cub::DeviceRadixSort::SortKeys(nullptr, tb, reinterpret_cast<long long*>(r1), reinterpret_cast<long long*>(r2),
+                                      k2, 0, 64, ctx->s));
     tmp_bytes = std::max(tmp_bytes, tb);
-    ENSURE(sort_tmp, std::max<size_t>(tmp_bytes, k + 64) + 64);
+    CK(cub::DeviceSelect::Unique(nullptr, tb, reinterpret_cast<long long*>(r2), reinterpret_cast<long long*>(r1), nsel,
+                                 k2, ctx->s));
+    tmp_bytes = std::max(tmp_bytes, tb);
+    ENSURE(sort_tmp, tmp_bytes + 64);
+    // 1. labels: sorted distinct endpoints of the non-loop edges
+    uint64_t e2 = 0;
     if (k) {
-        CK(cub::DeviceRadixSort::SortPairs(ctx->sort_tmp.p, tmp_bytes, b, b2, a, a2, (int)k, 0, 64, ctx->s));
-        CK(cub::DeviceRadixSort::SortPairs(ctx->sort_tmp.p, tmp_bytes, a2, a, b2, b, (int)k, 0, 64, ctx->s));
-        ctx->launches += 16;
-    }
-    // first of each (a, b) run, not a loop -> compact into (a2, b2)
-    auto* keep = reinterpret_cast<unsigned char*>(raw);  // k bytes
-    auto* nsel = reinterpret_cast<int*>(flags + 2);
-    if (k) {
-        k_first_of_run<<<grid, 256, 0, ctx->s>>>(k, a, b, keep);
+        k_loop_flags<<<grid_for(k, 256, big), 256, 0, ctx->s>>>(k, raw, r2, flags);
         LAUNCHED();
-    }
-    tb = 0;
-    CK(cub::DeviceSelect::Flagged(nullptr, tb, a, keep, a2, nsel, (int)k, ctx->s));
-    if (tb > ctx->sort_tmp.cap) ENSURE(sort_tmp, tb + 64);
-    if (k) {
-        CK(cub::DeviceSelect::Flagged(ctx->sort_tmp.p, tb, a, keep, a2, nsel, (int)k, ctx->s));
-        CK(cub::DeviceSelect::Flagged(ctx->sort_tmp.p, tb, b, keep, b2, nsel, (int)k, ctx->s));
-        ctx->launches += 4;
-    } else {
-        CK(cudaMemsetAsync(nsel, 0, sizeof(int), ctx->s));
-    }
-    int m_i = 0;
-    unsigned long long loops = 0;
-    CK(cudaMemcpyAsync(&m_i, nsel, sizeof(int), cudaMemcpyDeviceToHost, ctx->s));
-    CK(cudaMemcpyAsync(&loops, flags, 8, cudaMemcpyDeviceToHost, ctx->s));
-    CK(cudaStreamSynchronize(ctx->s));
-    const uint64_t m = (uint64_t)m_i;
-    // labels: sorted distinct endpoints of the kept edges
-    long long* ends = a;        // 2m <= 2k words over a, b
-    long long* ends_sorted = raw;  // raw's 2k words
-    if (m) {
-        k_interleave_endpoints<<<grid_for(m, 256, ctx->sms * 16), 256, 0, ctx->s>>>(m, a2, b2, ends);
-        LAUNCHED();
-        tb = 0;
-        CK(cub::DeviceRadixSort::SortKeys(nullptr, tb, ends, ends_sorted, (int)(2 * m), 0, 64, ctx->s));
-        if (tb > ctx->sort_tmp.cap) ENSURE(sort_tmp, tb + 64);
-        CK(cub::DeviceRadixSort::SortKeys(ctx->sort_tmp.p, tb, ends, ends_sorted, (int)(2 * m), 0, 64, ctx->s));
-        ctx->launches += 8;
-    }
-    ENSURE(labels, std::max<uint64_t>(2 * m, 1) * 8);
-    long long* lab = P<long long>(ctx->labels);
-    int n_i = 0;
-    if (m) {
-        tb = 0;
-        CK(cub::DeviceSelect::Unique(nullptr, tb, ends_sorted, lab, nsel, (int)(2 * m), ctx->s));
-        if (tb > ctx->sort_tmp.cap) ENSURE(sort_tmp, tb + 64);
-        CK(cub::DeviceSelect::Unique(ctx->sort_tmp.p, tb, ends_sorted, lab, nsel, (int)(2 * m), ctx->s));
-        ctx->launches += 2;
-        CK(cudaMemcpyAsync(&n_i, nsel, sizeof(int), cudaMemcpyDeviceToHost, ctx->s));
+        tb = ctx->sort_tmp.cap;
+        CK(cub::DeviceSelect::Flagged(ctx->sort_tmp.p, tb, raw, r2, reinterpret_cast<long long*>(r1), nsel, k2, ctx->s));
+        long long e2_i = 0;
+        CK(cudaMemcpyAsync(&e2_i, nsel, 8, cudaMemcpyDeviceToHost, ctx->s));
         CK(cudaStreamSynchronize(ctx->s));
+        e2 = static_cast<uint64_t>(e2_i);
+        ctx->launches += 3;
     }
-    const uint32_t n = (uint32_t)n_i;
-    // CSR: directed pair keys, one sort -> rows sorted; degrees -> offsets
+    unsigned long long loops = 0;
+    CK(cudaMemcpyAsync(&loops, flags, 8, cudaMemcpyDeviceToHost, ctx->s));
+    uint64_t n64 = 0;
+    if (e2) {
+        tb = ctx->sort_tmp.cap;
+        CK(cub::DeviceRadixSort::SortKeys(ctx->sort_tmp.p, tb, reinterpret_cast<long long*>(r1),
+                                          reinterpret_cast<long long*>(r2), static_cast<int64_t>(e2), 0, 64, ctx->s));
+        tb = ctx->sort_tmp.cap;
+        CK(cub::DeviceSelect::Unique(ctx->sort_tmp.p, tb, reinterpret_cast<long long*>(r2),
+                                     reinterpret_cast<long long*>(r1), nsel, static_cast<int64_t>(e2), ctx->s));
+        ctx->launches += 10;
+        long long n_i = 0;
+        CK(cudaMemcpyAsync(&n_i, nsel, 8, cudaMemcpyDeviceToHost, ctx->s));
+        CK(cudaStreamSynchronize(ctx->s));
+        n64 = static_cast<uint64_t>(n_i);
+    }
+    CK(cudaStreamSynchronize(ctx->s));
+    if (n64 > 0xFFF00000ull)  // the listing engine's limit (check_args)
+        return ctx->fail(TL_ERR_INVALID_ARGUMENT, "normalize: more than 2^32 - 2^20 distinct labels");
+    const uint32_t n = static_cast<uint32_t>(n64);
+    ENSURE(labels, std::max<uint64_t>(n, 1) * 8);
+    long long* lab = P<long long>(ctx->labels);
+    if (n) CK(cudaMemcpyAsync(lab, r1, (size_t)n * 8, cudaMemcpyDeviceToDevice, ctx->s));
+    // 2-3. one key per raw edge, sorted and deduplicated: the kept edges
+    const int hi_bits = 32 + std::max(1, 32 - __builtin_clz(std::max(n, 2u) - 1));
+    auto* ekeys = reinterpret_cast<unsigned long long*>(r1);
+    auto* esorted = reinterpret_cast<unsigned long long*>(r2);
+    auto* edges_u = reinterpret_cast<unsigned long long*>(r1);
+    uint64_t m = 0;
+    if (e2) {
+        k_edge_keys<<<grid_for(k, 256, big), 256, 0, ctx->s>>>(k, raw, lab, n, ekeys);
+        LAUNCHED();
+        tb = ctx->sort_tmp.cap;
+        CK(cub::DeviceRadixSort::SortKeys(ctx->sort_tmp.p, tb, ekeys, esorted, static_cast<int64_t>(k), 0, hi_bits,
+                                          ctx->s));
+        tb = ctx->sort_tmp.cap;
+        CK(cub::DeviceSelect::Unique(ctx->sort_tmp.p, tb, esorted, edges_u, nsel, static_cast<int64_t>(k), ctx->s));
+        ctx->launches += 10;
+        long long u_i = 0;
+        CK(cudaMemcpyAsync(&u_i, nsel, 8, cudaMemcpyDeviceToHost, ctx->s));
+        CK(cudaStreamSynchronize(ctx->s));
+        m = static_cast<uint64_t>(u_i) - (loops ? 1 : 0);  // the loop key sorts last
+    }
+    // 4. CSR: directed pair keys, one sort -> rows sorted; degrees -> offsets
     ENSURE(goff, ((size_t)n + 1) * 8);
     ENSURE(gadj, std::max<uint64_t>(2 * m, 1) * 4);
     ENSURE(outdeg, (size_t)std::max<uint32_t>(n, 1) * 4);
-    auto* keys = reinterpret_cast<unsigned long long*>(raw);       // 2m words (raw region: 2k >= 2m)
-    auto* keys2 = reinterpret_cast<unsigned long long*>(a);        // 2m words over a, b
+    auto* dkeys = reinterpret_cast<unsigned long long*>(raw);  // 2m <= 2k words
+    auto* dsorted = reinterpret_cast<unsigned long long*>(r2);
     if (n) CK(cudaMemsetAsync(ctx->outdeg.p, 0, (size_t)n * 4, ctx->s));
     if (m) {
-        k_dense_keys<<<grid_for(m, 256, ctx->sms * 16), 256, 0, ctx->s>>>(m, a2, b2, lab, n, keys,
-                                                                        P<uint32_t>(ctx->outdeg));
+        k_directed_keys<<<grid_for(m, 256, big), 256, 0, ctx->s>>>(m, edges_u, dkeys, P<uint32_t>(ctx->outdeg));
         LAUNCHED();
-        const int hi_bits = 32 + std::max(1, 32 - __builtin_clz(std::max(n, 2u) - 1));
-        tb = 0;
-        CK(cub::DeviceRadixSort::SortKeys(nullptr, tb, keys, keys2, (int)(2 * m), 0, hi_bits, ctx->s));
+        tb = ctx->sort_tmp.cap;
+        CK(cub::DeviceRadixSort::SortKeys(nullptr, tb, dkeys, dsorted, static_cast<int64_t>(2 * m), 0, hi_bits, ctx->s));
         if (tb > ctx->sort_tmp.cap) ENSURE(sort_tmp, tb + 64);
-        CK(cub::DeviceRadixSort::SortKeys(ctx->sort_tmp.p, tb, keys, keys2, (int)(2 * m), 0, hi_bits, ctx->s));
+        tb = ctx->sort_tmp.cap;
+        CK(cub::DeviceRadixSort::SortKeys(ctx->sort_tmp.p, tb, dkeys, dsorted, static_cast<int64_t>(2 * m), 0, hi_bits,
+                                          ctx->s));
         ctx->launches += 8;
-        k_low_words<<<grid_for(2 * m, 256, ctx->sms * 16), 256, 0, ctx->s>>>(2 * m, keys2, P<uint32_t>(ctx->gadj));
+        k_low_words<<<grid_for(2 * m, 256, big), 256, 0, ctx->s>>>(2 * m, dsorted, P<uint32_t>(ctx->gadj));
         LAUNCHED();
     }
     tl_status st = scan_offsets(ctx, n, P<uint32_t>(ctx->outdeg), P<uint64_t>(ctx->goff));

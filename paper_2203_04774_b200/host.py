@@ -269,6 +269,14 @@ def gen_rmat(scale: int, edge_factor: int = 16, seed: int = 1) -> Graph:
     return _gen(_native.trihost().th_gen_rmat, scale, edge_factor, seed)
 
 
+def gen_rmat_raw(scale: int, edge_factor: int = 16, seed: int = 1) -> np.ndarray:
+    """The raw (k, 2) int64 draws behind gen_rmat (loops and duplicates kept)."""
+    out = np.empty(((edge_factor << scale), 2), np.int64)
+    if _native.trihost().th_gen_rmat_raw(scale, edge_factor, seed, out.ctypes.data) != 0:
+        raise HostError(_th_err())
+    return out
+
+
 def gen_chung_lu(n: int, draws: int, exponent: float = 2.1, wmin: float = 2.0,
                  wmax: float = 50000.0, seed: int = 1) -> Graph:
     """Chung-Lu with Pareto(exponent, wmin) weights capped at wmax (C2)."""

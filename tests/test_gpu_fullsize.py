@@ -169,3 +169,43 @@ def test_full_size_counts_vs_reference(ctx, cfg):
                 (exp.triangle_count, exp.checksum, exp.inner_ops, exp.mark_ops), (cfg, meth, algo)
             assert np.array_equal(ctx.fetch_vertex_counts(g.n), exp.vcounts)
         del rv
+
+
+def test_c5_raw_edge_list_normalize():
+    """tl_normalize at C5 scale: the 2^31 raw R-MAT-27 draws (loops and
+    duplicates kept, more than 2^31 endpoints) through the device normalize
+    (graph.cpp:115-151 + from_dense_edges :13-56) give gen_rmat(27)'s graph
+    restricted to its non-isolated vertices: labels = those vertex ids,
+    degrees and rows equal after mapping dense ids back through the labels;
+    the device-resident graph then orients and lists C5's triangles."""
+    raw = host.gen_rmat_raw(27, 16, 1)
+    k = raw.shape[0]
+    assert 2 * k > 2**31
+    loops_expected = int(np.count_nonzero(raw[:, 0] == raw[:, 1]))
+    c = tg.Context(0)
+    try:
+        n, m, lo, du = c.normalize(raw)
+        del raw
+        g = tg.gen_rmat(27, 16, 1)
+        deg = np.diff(g.offsets.astype(np.int64))
+        assert (m, lo, du) == (g.m, loops_expected, k - loops_expected - g.m)
+        off, adj, labels = c.fetch_graph()
+        assert np.array_equal(labels, np.flatnonzero(deg))
+        assert np.array_equal(np.diff(off.astype(np.int64)), deg[labels])
+        step = 1 << 28
+        for i in range(0, adj.shape[0], step):
+            assert np.array_equal(labels[adj[i:i + step]], g.adjacency[i:i + step].astype(np.int64)), i
+        del off, adj
+        c.orient_normalized("degree")
+        st = c.list(TL_ALGO_APM, TL_OUT_CHECKSUM)
+    finally:
+        c.close()
+    # isolated vertices carry no triangles, and the checksum hashes dense ids of
+    # the normalized graph: compare counts with the full C5 listing
+    c2 = tg.Context(0)
+    try:
+        c2.orient(g.offsets, g.adjacency, degree_ranks_numpy(g.offsets))
+        full = c2.list(TL_ALGO_APM, 0)
+    finally:
+        c2.close()
+    assert st.triangle_count == full.triangle_count
