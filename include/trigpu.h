@@ -100,12 +100,29 @@ TL_API tl_status tl_orient_device(tl_ctx* ctx, uint32_t n, uint64_t m, const uin
  * Graph CSR. tl_order: host arrays in and out; tl_order_device: device
  * arrays. Replaces degree_order / split_order (ordering.hpp) on the listing
  * path; the other orderings stay the reference's host code. */
-enum { TL_ORDER_DEGREE = 0, TL_ORDER_SPLIT = 1 };
+enum { TL_ORDER_DEGREE = 0, TL_ORDER_SPLIT = 1, TL_ORDER_CORE = 2 };
 TL_API tl_status tl_order(tl_ctx* ctx, uint32_t n, const uint64_t* offsets, int method, uint32_t* rank);
 TL_API tl_status tl_order_device(tl_ctx* ctx, uint32_t n, const uint64_t* d_offsets, int method, uint32_t* d_rank);
+/* k-core decomposition on the device: replaces
+ * core_decompose / core_order (ordering.cpp:141-188; CoreDecomposition,
+ * ordering.hpp:56-64). coreness[v] and the degeneracy equal the reference's
+ * bit for bit. rank[v] is a degeneracy ordering with the reference order's
+ * defining property (every vertex has at most coreness(v) successors, so
+ * max d+ = degeneracy): vertices sorted by (removal round of the level-
+ * synchronous peel, id). The reference's bucket queue removes one vertex at a
+ * time and breaks ties by the history of its swaps; that sequence is not
+ * reproduced (csrc/core.cuh says why), so rank differs from core_order(g)
+ * among ties while every listing result is unchanged. rank / coreness may be
+ * NULL. tl_core_decompose: host arrays; _device: device arrays. */
+TL_API tl_status tl_core_decompose(tl_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* offsets, const uint32_t* adj,
+                                   uint32_t* rank, uint32_t* coreness, uint32_t* degeneracy);
+TL_API tl_status tl_core_decompose_device(tl_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* d_offsets,
+                                          const uint32_t* d_adj, uint32_t* d_rank, uint32_t* d_coreness,
+                                          uint32_t* degeneracy);
 /* tl_orient with the ordering computed on the device by `method`
- * (TL_ORDER_DEGREE / TL_ORDER_SPLIT): the whole path from the host Graph CSR,
- * no host ordering. The ranks can be read back with tl_fetch_ranks. */
+ * (TL_ORDER_DEGREE / TL_ORDER_SPLIT / TL_ORDER_CORE): the whole path from the
+ * host Graph CSR, no host ordering. The ranks can be read back with
+ * tl_fetch_ranks. */
 TL_API tl_status tl_orient_ordered(tl_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* offsets,
                                    const uint32_t* adj, int method);
 TL_API tl_status tl_fetch_ranks(tl_ctx* ctx, uint32_t* rank);

@@ -90,6 +90,32 @@ inline trilist::Ordering split_order(const trilist::Graph& g, Context& ctx = def
     return device_order(g, TL_ORDER_SPLIT, ctx);
 }
 
+// core_decompose (ordering.cpp:141-188) on the GPU. coreness and degeneracy
+// equal the reference's; `order` is a degeneracy ordering ((peel round, id)
+// ascending, see trigpu.h), not the reference's swap-dependent sequence.
+inline trilist::CoreDecomposition core_decompose(const trilist::Graph& g, Context& ctx = default_context()) {
+    const VertexId n = g.vertex_count();
+    std::vector<std::uint64_t> off(static_cast<std::size_t>(n) + 1, 0);
+    std::vector<VertexId> adj;
+    adj.reserve(2 * g.edge_count());
+    for (VertexId u = 0; u < n; ++u) {
+        off[u + 1] = off[u] + g.degree(u);
+        for (VertexId v : g.neighbors(u)) adj.push_back(v);
+    }
+    std::vector<VertexId> rank(n);
+    trilist::CoreDecomposition out;
+    out.coreness.assign(n, 0);
+    std::uint32_t dg = 0;
+    ctx.check(tl_core_decompose(ctx.get(), n, g.edge_count(), off.data(), adj.data(), rank.data(),
+                                out.coreness.data(), &dg));
+    out.degeneracy = dg;
+    out.order = trilist::Ordering::from_ranks(std::move(rank));
+    return out;
+}
+inline trilist::Ordering core_order(const trilist::Graph& g, Context& ctx = default_context()) {
+    return core_decompose(g, ctx).order;
+}
+
 // GPU-resident OrientedView (oriented_view.hpp:17-50). The device holds one
 // view per Context; constructing another view in the same context replaces it
 // (each listing call re-orients if needed).

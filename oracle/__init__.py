@@ -63,6 +63,8 @@ def lib() -> C.CDLL:
     L.or_orient_parallel.restype = C.c_int
     L.or_sort_triples.argtypes = [_vp, _u64, C.c_int]
     L.or_sort_triples.restype = None
+    L.or_core_decompose.argtypes = [_u32, _vp, _vp, _vp, _vp]
+    L.or_core_decompose.restype = _u32
     return L
 
 
@@ -94,6 +96,8 @@ def ref() -> C.CDLL:
     L.ref_graph_csr.argtypes = [_vp, _vp, _vp]
     L.ref_order.argtypes = [_vp, C.c_char_p, _u64, _vp]
     L.ref_order.restype = C.c_int
+    L.ref_core_decompose.argtypes = [_vp, _vp, _vp]
+    L.ref_core_decompose.restype = C.c_int64
     L.ref_cost.argtypes = [_vp, _vp, _vp]
     L.ref_cost.restype = C.c_int
     L.ref_view.argtypes = [_vp, _vp, _u32]
@@ -229,6 +233,17 @@ def cost(view: OrientedCSR) -> tuple[int, int, int, int]:
     return tuple(int(x) for x in out)
 
 
+def core_decompose(offsets: np.ndarray, adj: np.ndarray) -> tuple[np.ndarray, np.ndarray, int]:
+    """or_core_decompose <- ordering.cpp:141-188: (ranks of the removal order, coreness, degeneracy)."""
+    offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+    adj = np.ascontiguousarray(adj if adj.shape[0] else np.zeros(1, np.uint32), dtype=np.uint32)
+    n = offsets.shape[0] - 1
+    rank = np.zeros(max(n, 1), np.uint32)
+    core = np.zeros(max(n, 1), np.uint32)
+    dg = lib().or_core_decompose(n, offsets.ctypes.data, adj.ctypes.data, rank.ctypes.data, core.ctypes.data)
+    return rank[:n], core[:n], int(dg)
+
+
 def brute(offsets: np.ndarray, adj: np.ndarray) -> np.ndarray:
     """or_brute <- oracle.cpp:12-30 (sorted u<v<w triples)."""
     n = offsets.shape[0] - 1
@@ -332,6 +347,15 @@ class RefGraph:
         if ref().ref_order(self.h, method.encode(), seed, r.ctypes.data) != 0:
             raise ValueError(ref().ref_last_error().decode())
         return r[: self.n]
+
+    def core_decompose(self) -> tuple[np.ndarray, np.ndarray, int]:
+        """The reference's core_decompose(g): (ranks, coreness, degeneracy)."""
+        r = np.zeros(max(self.n, 1), np.uint32)
+        c = np.zeros(max(self.n, 1), np.uint32)
+        dg = ref().ref_core_decompose(self.h, r.ctypes.data, c.ctypes.data)
+        if dg < 0:
+            raise ValueError(ref().ref_last_error().decode())
+        return r[: self.n], c[: self.n], int(dg)
 
     def cost(self, rank) -> tuple[int, int, int, int]:
         rank = np.ascontiguousarray(rank, dtype=np.uint32)

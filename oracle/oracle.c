@@ -343,3 +343,62 @@ void or_canonicalize(uint32_t* tri, uint64_t k) {
     }
     qsort(tri, (size_t)k, 3 * sizeof(uint32_t), cmp_triple);
 }
+
+/* ---- core_decompose (ordering.cpp:141-188) ---------------------------------
+ * vert holds the vertices sorted by current degree, pos their positions, bin
+ * the first position of each degree bucket; a decrement of u swaps u with the
+ * first vertex of its bucket and moves the bucket boundary past it
+ * (ordering.cpp:170-181), so the removal sequence depends on the swap history
+ * exactly as in the reference. */
+uint32_t or_core_decompose(uint32_t n, const uint64_t* offsets, const uint32_t* adj, uint32_t* rank,
+                           uint32_t* coreness) {
+    if (n == 0) return 0;
+    uint32_t max_deg = 0;
+    uint32_t* deg = (uint32_t*)malloc(sizeof(uint32_t) * n);
+    uint32_t* vert = (uint32_t*)malloc(sizeof(uint32_t) * n);
+    uint32_t* pos = (uint32_t*)malloc(sizeof(uint32_t) * n);
+    for (uint32_t v = 0; v < n; ++v) {
+        deg[v] = (uint32_t)(offsets[v + 1] - offsets[v]);
+        if (deg[v] > max_deg) max_deg = deg[v];
+    }
+    const size_t nb = (size_t)max_deg + 2;
+    uint64_t* bin = (uint64_t*)calloc(nb, sizeof(uint64_t));
+    uint64_t* cursor = (uint64_t*)malloc(sizeof(uint64_t) * nb);
+    for (uint32_t v = 0; v < n; ++v) ++bin[deg[v] + 1]; /* :150-153 */
+    for (size_t d = 1; d < nb; ++d) bin[d] += bin[d - 1]; /* :154 */
+    memcpy(cursor, bin, sizeof(uint64_t) * nb);
+    for (uint32_t v = 0; v < n; ++v) { /* :156-160 */
+        pos[v] = (uint32_t)cursor[deg[v]];
+        vert[cursor[deg[v]]++] = v;
+    }
+    uint32_t degeneracy = 0;
+    for (uint32_t step = 0; step < n; ++step) { /* :166-184 */
+        const uint32_t v = vert[step];
+        if (rank) rank[v] = step;
+        if (coreness) coreness[v] = deg[v];
+        if (deg[v] > degeneracy) degeneracy = deg[v];
+        for (uint64_t e = offsets[v]; e < offsets[v + 1]; ++e) {
+            const uint32_t u = adj[e];
+            if (deg[u] <= deg[v]) continue;
+            const uint32_t du = deg[u];
+            const uint32_t first_pos = (uint32_t)bin[du];
+            const uint32_t first_vert = vert[first_pos];
+            if (u != first_vert) {
+                const uint32_t pu = pos[u];
+                vert[pu] = first_vert;
+                vert[first_pos] = u;
+                pos[u] = first_pos;
+                pos[first_vert] = pu;
+            }
+            ++bin[du];
+            --deg[u];
+        }
+        ++bin[deg[v]];
+    }
+    free(deg);
+    free(vert);
+    free(pos);
+    free(bin);
+    free(cursor);
+    return degeneracy;
+}

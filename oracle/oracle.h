@@ -81,6 +81,13 @@ void or_cost(uint32_t n, const uint64_t* succ_off, const uint64_t* pred_off, uin
 uint64_t or_brute(uint32_t n, const uint64_t* offsets, const uint32_t* adj, uint32_t* tri,
                   uint64_t cap);
 
+/* core_decompose (core/src/ordering.cpp:141-188): Batagelj-Zaversnik bucket
+ * peeling, restated line for line - rank[v] = removal step of v (the
+ * reference's core_order, swap for swap), coreness[v] = degree at removal;
+ * returns the degeneracy. Checker for tl_core_decompose's coreness. */
+uint32_t or_core_decompose(uint32_t n, const uint64_t* offsets, const uint32_t* adj, uint32_t* rank,
+                           uint32_t* coreness);
+
 /* Canonical form (listing.hpp:57-62): sort ids inside each triple, then sort
  * the triple list lexicographically. In place. */
 void or_canonicalize(uint32_t* tri, uint64_t k);

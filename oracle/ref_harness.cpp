@@ -277,6 +277,21 @@ int ref_order(void* gp, const char* method, std::uint64_t seed, std::uint32_t* r
     }
 }
 
+// core_decompose (ordering.cpp:141-188): ranks of the removal order, coreness; returns the
+// degeneracy (-1 on error).
+std::int64_t ref_core_decompose(void* gp, std::uint32_t* rank_out, std::uint32_t* coreness_out) {
+    try {
+        const Graph& g = *static_cast<Graph*>(gp);
+        const CoreDecomposition cd = core_decompose(g);
+        if (rank_out) std::memcpy(rank_out, cd.order.ranks().data(), sizeof(VertexId) * cd.order.size());
+        if (coreness_out) std::memcpy(coreness_out, cd.coreness.data(), sizeof(VertexId) * cd.coreness.size());
+        return cd.degeneracy;
+    } catch (const std::exception& e) {
+        g_error = e.what();
+        return -1;
+    }
+}
+
 int ref_cost(void* gp, const std::uint32_t* rank, std::uint64_t out[4]) {
     try {
         const Graph& g = *static_cast<Graph*>(gp);

@@ -31,6 +31,7 @@ TL_ALGO_APP = 0
 TL_ALGO_APM = 1
 TL_ORDER_DEGREE = 0
 TL_ORDER_SPLIT = 1
+TL_ORDER_CORE = 2
 TL_OUT_COUNT = 0
 TL_OUT_CHECKSUM = 1
 TL_OUT_VERTEX_COUNTS = 2
@@ -49,6 +50,7 @@ TRIGPU_SYMBOLS = (
     "tl_timer_start", "tl_timer_stop", "tl_order", "tl_order_device", "tl_orient_ordered",
     "tl_fetch_ranks", "tl_normalize", "tl_fetch_graph", "tl_orient_normalized",
     "tl_fetch_triangles_range", "tl_fetch_triangle_labels", "tl_debug_set", "tl_list_range",
+    "tl_core_decompose", "tl_core_decompose_device",
 )
 
 
@@ -143,6 +145,10 @@ def trigpu() -> C.CDLL:
     lib.tl_order_device.restype = C.c_int
     lib.tl_orient_ordered.argtypes = [_vp, _u32, _u64, _vp, _vp, C.c_int]
     lib.tl_orient_ordered.restype = C.c_int
+    lib.tl_core_decompose.argtypes = [_vp, _u32, _u64, _vp, _vp, _vp, _vp, C.POINTER(_u32)]
+    lib.tl_core_decompose.restype = C.c_int
+    lib.tl_core_decompose_device.argtypes = [_vp, _u32, _u64, _vp, _vp, _vp, _vp, C.POINTER(_u32)]
+    lib.tl_core_decompose_device.restype = C.c_int
     lib.tl_fetch_ranks.argtypes = [_vp, _vp]
     lib.tl_fetch_ranks.restype = C.c_int
     lib.tl_normalize.argtypes = [_vp, _u64, _vp, C.POINTER(_u32), C.POINTER(_u64), C.POINTER(_u64),

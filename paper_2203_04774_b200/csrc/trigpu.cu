@@ -29,6 +29,7 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_select.cuh>
 
+#include "core.cuh"
 #include "normalize.cuh"
 #include "orient.cuh"
 #include "segsort.cuh"
@@ -711,6 +712,8 @@ TL_API tl_status tl_orient(tl_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* 
 
 // Degree / split order on the device into d_rank (device, n entries).
 static tl_status order_core(tl_ctx* ctx, uint32_t n, const uint64_t* d_off, int method, uint32_t* d_rank) {
+    if (method == TL_ORDER_CORE)
+        return ctx->fail(TL_ERR_INVALID_ARGUMENT, "order: TL_ORDER_CORE needs the adjacency (tl_core_decompose)");
     if (method != TL_ORDER_DEGREE && method != TL_ORDER_SPLIT)
         return ctx->fail(TL_ERR_INVALID_ARGUMENT, "order: method must be TL_ORDER_DEGREE or TL_ORDER_SPLIT");
     if (!n) return TL_OK;
@@ -729,6 +732,118 @@ static tl_status order_core(tl_ctx* ctx, uint32_t n, const uint64_t* d_off, int 
     k_rank_from_sequence<<<grid_for(n, 256, ctx->sms * 16), 256, 0, ctx->s>>>(n, v_out, method == TL_ORDER_SPLIT,
                                                                                d_rank);
     LAUNCHED();
+    return TL_OK;
+}
+
+// core_decompose (ordering.cpp:141-188) on the device: coreness into `indeg`
+// (n words), the degeneracy order's ranks into d_rank, level-synchronous
+// peeling (core.cuh). d_off / d_adj: the Graph CSR on the device.
+static tl_status core_order_core(tl_ctx* ctx, uint32_t n, const uint64_t* d_off, const uint32_t* d_adj,
+                                 uint32_t* d_rank, uint32_t* degeneracy) {
+    if (degeneracy) *degeneracy = 0;
+    if (!n) return TL_OK;
+    ENSURE(lists, (size_t)n * 4 * kClasses);
+    ENSURE(outdeg, (size_t)n * 4 + 4);
+    ENSURE(indeg, (size_t)n * 4 + 4);
+    ENSURE(small, 128);
+    uint32_t* L = P<uint32_t>(ctx->lists);
+    uint32_t *alive = L, *kept = L + n, *f0 = L + 2 * (uint64_t)n, *f1 = L + 3 * (uint64_t)n;
+    CoreState S{d_off, d_adj, P<uint32_t>(ctx->outdeg), L + 4 * (uint64_t)n, P<uint32_t>(ctx->indeg)};
+    auto* acc = static_cast<unsigned int*>(ctx->small.p);  // [0] frontier, [1] kept, [2] min kept degree, [4..5] small-kernel state
+    const unsigned big = ctx->sms * 16;
+    k_core_init<<<grid_for(n, 256, big), 256, 0, ctx->s>>>(n, S, alive);
+    LAUNCHED();
+    uint32_t k = 0, r = 0, nalive = n, maxcore = 0;
+    unsigned int h[8];
+    while (nalive) {
+        const unsigned int init[3] = {0u, 0u, kNone};
+        CK(cudaMemcpyAsync(acc, init, sizeof init, cudaMemcpyHostToDevice, ctx->s));
+        k_core_scan<<<grid_for(nalive, 256, big), 256, 0, ctx->s>>>(alive, nalive, S, k, r, f0, kept, acc);
+        LAUNCHED();
+        CK(cudaMemcpyAsync(h, acc, 12, cudaMemcpyDeviceToHost, ctx->s));
+        CK(cudaStreamSynchronize(ctx->s));
+        std::swap(alive, kept);
+        nalive = h[1];
+        uint32_t count = h[0];
+        if (!count) {  // empty level: jump to the smallest remaining degree
+            if (nalive) k = h[2];
+            continue;
+        }
+        maxcore = k;
+        ++r;
+        uint32_t *cur = f0, *nxt = f1;
+        while (count) {
+            if (count <= kCoreQ) {
+                k_core_peel_small<<<1, 1024, 0, ctx->s>>>(cur, count, S, k, r, nxt, acc + 4);
+                LAUNCHED();
+                CK(cudaMemcpyAsync(h, acc + 4, 8, cudaMemcpyDeviceToHost, ctx->s));
+                CK(cudaStreamSynchronize(ctx->s));
+                r += h[0];
+                count = h[1];
+            } else {
+                CK(cudaMemsetAsync(acc, 0, 4, ctx->s));
+                k_core_peel<<<grid_for((uint64_t)count * 32, 256, big), 256, 0, ctx->s>>>(cur, count, S, k, r, nxt, acc);
+                LAUNCHED();
+                CK(cudaMemcpyAsync(h, acc, 4, cudaMemcpyDeviceToHost, ctx->s));
+                CK(cudaStreamSynchronize(ctx->s));
+                ++r;
+                count = h[0];
+            }
+            std::swap(cur, nxt);
+        }
+        ++k;
+    }
+    if (degeneracy) *degeneracy = maxcore;
+    // order = (removal round, id) ascending: one stable radix sort of the ids by round
+    uint32_t *v_in = L, *k_out = L + n, *v_out = L + 2 * (uint64_t)n;
+    k_core_iota<<<grid_for(n, 256, big), 256, 0, ctx->s>>>(n, v_in);
+    LAUNCHED();
+    int bits = 1;
+    while (bits < 32 && (r >> bits)) ++bits;
+    size_t tmp_bytes = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, S.rnd, k_out, v_in, v_out, (int)n, 0, bits, ctx->s));
+    ENSURE(sort_tmp, tmp_bytes + 16);
+    CK(cub::DeviceRadixSort::SortPairs(ctx->sort_tmp.p, tmp_bytes, S.rnd, k_out, v_in, v_out, (int)n, 0, bits, ctx->s));
+    ctx->launches += 2 * ((bits + 7) / 8);
+    k_rank_from_sequence<<<grid_for(n, 256, big), 256, 0, ctx->s>>>(n, v_out, false, d_rank);
+    LAUNCHED();
+    return TL_OK;
+}
+
+TL_API tl_status tl_core_decompose_device(tl_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* d_offsets,
+                                          const uint32_t* d_adj, uint32_t* d_rank, uint32_t* d_coreness,
+                                          uint32_t* degeneracy) {
+    if (!ctx || (n && (!d_offsets || !d_rank)) || (m && !d_adj)) return TL_ERR_INVALID_ARGUMENT;
+    if (n == 0xFFFFFFFFu) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "core_decompose: n must be < 2^32 - 1");
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return ctx->cuda_fail("cudaSetDevice", cudaGetLastError());
+    ctx->oriented = false;  // outdeg / indeg / lists are reused
+    drop_results(ctx);
+    tl_status st = core_order_core(ctx, n, d_offsets, d_adj, d_rank, degeneracy);
+    if (st != TL_OK) return st;
+    if (n && d_coreness) CK(cudaMemcpyAsync(d_coreness, ctx->indeg.p, (size_t)n * 4, cudaMemcpyDeviceToDevice, ctx->s));
+    CK(cudaStreamSynchronize(ctx->s));
+    return TL_OK;
+}
+
+TL_API tl_status tl_core_decompose(tl_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* offsets, const uint32_t* adj,
+                                   uint32_t* rank, uint32_t* coreness, uint32_t* degeneracy) {
+    tl_status st = check_args(ctx, n, m, offsets, adj, nullptr, false);
+    if (st != TL_OK) return st;
+    if (n && offsets[0] != 0) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "core_decompose: offsets[0] must be 0");
+    if (n && offsets[n] != 2 * m) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "core_decompose: offsets[n] must equal 2m");
+    ctx->normalized = false;  // goff / gadj are overwritten
+    ctx->oriented = false;
+    drop_results(ctx);
+    ENSURE(goff, ((size_t)n + 1) * 8);
+    ENSURE(gadj, 2 * m * 4);
+    ENSURE(rank, (size_t)n * 4 + 4);
+    CK(cudaMemcpyAsync(ctx->goff.p, offsets, ((size_t)n + 1) * 8, cudaMemcpyHostToDevice, ctx->s));
+    if (m) CK(cudaMemcpyAsync(ctx->gadj.p, adj, 2 * m * 4, cudaMemcpyHostToDevice, ctx->s));
+    st = core_order_core(ctx, n, P<uint64_t>(ctx->goff), P<uint32_t>(ctx->gadj), P<uint32_t>(ctx->rank), degeneracy);
+    if (st != TL_OK) return st;
+    if (n && rank) CK(cudaMemcpyAsync(rank, ctx->rank.p, (size_t)n * 4, cudaMemcpyDeviceToHost, ctx->s));
+    if (n && coreness) CK(cudaMemcpyAsync(coreness, ctx->indeg.p, (size_t)n * 4, cudaMemcpyDeviceToHost, ctx->s));
+    CK(cudaStreamSynchronize(ctx->s));
     return TL_OK;
 }
 
@@ -773,7 +888,9 @@ TL_API tl_status tl_orient_ordered(tl_ctx* ctx, uint32_t n, uint64_t m, const ui
     CK(cudaEventRecord(ctx->ev[PH_COUNT + 2], ctx->s));
     CK(cudaMemcpyAsync(ctx->goff.p, offsets, ((size_t)n + 1) * 8, cudaMemcpyHostToDevice, ctx->s));
     if (m) CK(cudaMemcpyAsync(ctx->gadj.p, adj, 2 * m * 4, cudaMemcpyHostToDevice, ctx->s));
-    st = order_core(ctx, n, P<uint64_t>(ctx->goff), method, P<uint32_t>(ctx->rank));
+    st = method == TL_ORDER_CORE
+             ? core_order_core(ctx, n, P<uint64_t>(ctx->goff), P<uint32_t>(ctx->gadj), P<uint32_t>(ctx->rank), nullptr)
+             : order_core(ctx, n, P<uint64_t>(ctx->goff), method, P<uint32_t>(ctx->rank));
     if (st != TL_OK) return st;
     CK(cudaEventRecord(ctx->ev[PH_H2D], ctx->s));
     st = orient_core(ctx, n, m, P<uint64_t>(ctx->goff), P<uint32_t>(ctx->gadj), P<uint32_t>(ctx->rank));
@@ -927,7 +1044,9 @@ TL_API tl_status tl_orient_normalized(tl_ctx* ctx, int method) {
     tl_status st = check_args(ctx, n, ctx->norm_m, ctx->goff.p, ctx->gadj.p, nullptr, false);
     if (st != TL_OK) return st;
     ENSURE(rank, (size_t)n * 4 + 4);
-    st = order_core(ctx, n, P<uint64_t>(ctx->goff), method, P<uint32_t>(ctx->rank));
+    st = method == TL_ORDER_CORE
+             ? core_order_core(ctx, n, P<uint64_t>(ctx->goff), P<uint32_t>(ctx->gadj), P<uint32_t>(ctx->rank), nullptr)
+             : order_core(ctx, n, P<uint64_t>(ctx->goff), method, P<uint32_t>(ctx->rank));
     if (st != TL_OK) return st;
     CK(cudaEventRecord(ctx->ev[PH_H2D], ctx->s));
     st = orient_core(ctx, n, ctx->norm_m, P<uint64_t>(ctx->goff), P<uint32_t>(ctx->gadj), P<uint32_t>(ctx->rank));

@@ -95,6 +95,7 @@ class Context:
 
     # device orderings (degree_order / split_order, ordering.cpp:66-109)
     _ORDERS = {"degree": _native.TL_ORDER_DEGREE, "split": _native.TL_ORDER_SPLIT}
+    _ORIENT_ORDERS = {**_ORDERS, "core": _native.TL_ORDER_CORE}  # core needs the adjacency
 
     def order(self, offsets: np.ndarray, method: str) -> np.ndarray:
         """Ordering::ranks() of degree_order / split_order, computed on the GPU."""
@@ -107,18 +108,33 @@ class Context:
                                                   rank.ctypes.data))
         return rank[:n]
 
+    def core_decompose(self, offsets: np.ndarray, adj: np.ndarray) -> tuple[np.ndarray, np.ndarray, int]:
+        """core_decompose(g) (ordering.cpp:141-188) on the GPU: (ranks of a degeneracy
+        ordering, coreness, degeneracy). Coreness / degeneracy equal the reference's; the
+        order is (peel round, id) - see include/trigpu.h."""
+        offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+        adj = np.ascontiguousarray(adj, dtype=np.uint32)
+        n = offsets.shape[0] - 1
+        rank = np.empty(max(n, 1), dtype=np.uint32)
+        core = np.empty(max(n, 1), dtype=np.uint32)
+        dg = C.c_uint32(0)
+        _check(self._p, _native.trigpu().tl_core_decompose(self._p, n, adj.shape[0] // 2, offsets.ctypes.data,
+                                                           adj.ctypes.data, rank.ctypes.data, core.ctypes.data,
+                                                           C.byref(dg)))
+        return rank[:n], core[:n], int(dg.value)
+
     def order_device(self, n: int, d_offsets: int, method: str, d_rank: int) -> None:
         _check(self._p, _native.trigpu().tl_order_device(self._p, n, d_offsets, self._ORDERS[method], d_rank))
 
     def orient_ordered(self, offsets: np.ndarray, adj: np.ndarray, method: str) -> None:
         """tl_orient with the ordering computed on the device (no host ordering)."""
-        if method not in self._ORDERS:
-            raise ValueError(f"orient_ordered: device orderings are {sorted(self._ORDERS)}")
+        if method not in self._ORIENT_ORDERS:
+            raise ValueError(f"orient_ordered: device orderings are {sorted(self._ORIENT_ORDERS)}")
         offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
         adj = np.ascontiguousarray(adj, dtype=np.uint32)
         _check(self._p, _native.trigpu().tl_orient_ordered(self._p, offsets.shape[0] - 1, adj.shape[0] // 2,
                                                            offsets.ctypes.data, adj.ctypes.data,
-                                                           self._ORDERS[method]))
+                                                           self._ORIENT_ORDERS[method]))
 
     def normalize(self, raw_pairs) -> tuple[int, int, int, int]:
         """Raw labeled edges -> Graph CSR on the device (normalize, graph.cpp:115-151).
@@ -160,7 +176,7 @@ class Context:
             first += k.value
 
     def orient_normalized(self, method: str) -> None:
-        _check(self._p, _native.trigpu().tl_orient_normalized(self._p, self._ORDERS[method]))
+        _check(self._p, _native.trigpu().tl_orient_normalized(self._p, self._ORIENT_ORDERS[method]))
 
     def fetch_ranks(self, n: int) -> np.ndarray:
         rank = np.empty(max(n, 1), dtype=np.uint32)

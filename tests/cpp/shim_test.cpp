@@ -198,6 +198,28 @@ int main() {
     }
     section("device degree / split orderings (ordering.cpp:66-109)", f0);
 
+    f0 = g_fail;  // device k-core decomposition vs core_decompose (ordering.cpp:141-188)
+    {
+        auto check = [&](const Graph& g, const std::string& tag) {
+            const CoreDecomposition a = trigpu::core_decompose(g), b = core_decompose(g);
+            expect(a.coreness == b.coreness, "device coreness " + tag);
+            expect(a.degeneracy == b.degeneracy, "device degeneracy " + tag);
+            const OrientedView v(g, a.order);  // the reference's own view under the device order
+            VertexId max_out = 0;
+            bool ok = true;
+            for (VertexId u = 0; u < g.vertex_count(); ++u) {
+                max_out = std::max(max_out, v.out_degree(u));
+                ok = ok && v.out_degree(u) <= b.coreness[u];
+            }
+            expect(ok, "d+ <= coreness under the device core order " + tag);
+            expect(max_out <= b.degeneracy, "max d+ <= degeneracy " + tag);
+        };
+        for (std::uint64_t seed = 0; seed < 40; ++seed)
+            check(random_small_graph(seed, 60, 400), "seed " + std::to_string(seed));
+        check(gen_gnm(100000, 1000000, 4242), "C1");
+    }
+    section("device core decomposition (ordering.cpp:141-188)", f0);
+
     f0 = g_fail;  // acceptance criteria 1-3
     {
         const int c0 = g_fail;

@@ -338,6 +338,83 @@ def test_device_orderings_match_reference(meth):
         c.close()
 
 
+def _succ_counts(g, rank):
+    """d+ per vertex under pi: neighbours of larger rank."""
+    src = np.repeat(np.arange(g.n, dtype=np.int64), np.diff(g.offsets.astype(np.int64)))
+    later = rank[g.adjacency] > rank[src]
+    return np.bincount(src[later], minlength=g.n)
+
+
+def test_device_core_decompose():
+    """tl_core_decompose: coreness and degeneracy equal core_decompose
+    (ordering.cpp:141-188; oracle.core_decompose is pinned to it swap for swap);
+    the ranks are a permutation with the degeneracy-order property d+(v) <=
+    coreness(v) (so max d+ = degeneracy, as under the reference's core order),
+    monotone in coreness; listing under it gives the reference's results."""
+    c = tg.Context(0)
+    try:
+        path = host.Graph(*_path_csr(30000))
+        graphs = [tg.gen_gnm(1, 0, 1), tg.gen_gnm(5, 0, 1), tg.gen_gnm(60, 400, 11), path,
+                  tg.gen_gnm(100000, 1000000, 4242), tg.gen_rmat(16, 16, 2), tg.gen_chung_lu(200000, 3000000, seed=3),
+                  tg.gen_ws(50000, 16, 0.1, seed=5), _hub_graph()]
+        for case in cases():
+            off, adj = case_csr(case)
+            graphs.append(host.Graph(off, adj))
+        for g in graphs:
+            rank, core, dg = c.core_decompose(g.offsets, g.adjacency)
+            r0, c0, d0 = oracle.core_decompose(g.offsets, g.adjacency)
+            assert np.array_equal(core, c0) and dg == d0
+            assert np.array_equal(np.sort(rank), np.arange(g.n, dtype=np.uint32))
+            dplus = _succ_counts(g, rank.astype(np.int64))
+            assert np.all(dplus <= core)
+            assert int(dplus.max(initial=0)) <= dg
+            order = np.argsort(rank)
+            assert np.all(np.diff(core[order].astype(np.int64)) >= 0)  # peeled level by level
+            # same listing results as under the reference's own core order
+            c.orient_ordered(g.offsets, g.adjacency, "core")
+            assert np.array_equal(c.fetch_ranks(g.n), rank)
+            for algo in (TL_ALGO_APM, TL_ALGO_APP):
+                st = c.list(algo, TL_OUT_CHECKSUM | TL_OUT_VERTEX_COUNTS)
+                vc = c.fetch_vertex_counts(g.n)
+                view = oracle.orient(g.offsets, g.adjacency, r0)
+                exp = oracle.list_triangles(view, algo, threads=8, vcounts=True)
+                assert (st.triangle_count, st.checksum) == (exp.triangle_count, exp.checksum)
+                assert np.array_equal(vc, exp.vcounts)
+        with pytest.raises(ValueError):
+            c.order(graphs[2].offsets, "core")  # offsets only: core needs the adjacency
+    finally:
+        c.close()
+
+
+def _path_csr(n):
+    """Path 0-1-...-(n-1): level 1 peels it from both ends, n/2 rounds."""
+    deg = np.full(n, 2, np.uint64)
+    deg[0] = deg[-1] = 1
+    off = np.zeros(n + 1, np.uint64)
+    off[1:] = np.cumsum(deg)
+    adj = np.empty(2 * (n - 1), np.uint32)
+    k = 0
+    for v in range(n):
+        if v > 0:
+            adj[k] = v - 1
+            k += 1
+        if v < n - 1:
+            adj[k] = v + 1
+            k += 1
+    return off, adj
+
+
+def _hub_graph():
+    """A 40-clique whose members also own 3000 leaves each (long rows, high levels)."""
+    k, leaves = 40, 3000
+    e = [(a, b) for a in range(k) for b in range(a + 1, k)]
+    nxt = k
+    for a in range(k):
+        e += [(a, nxt + i) for i in range(leaves)]
+        nxt += leaves
+    return tg.Graph.from_dense_edges(nxt, np.array(e, np.uint32))
+
+
 def test_device_normalize_matches_reference():
     """tl_normalize (raw labeled edges -> Graph CSR on the GPU) equals the
     reference's normalize (graph.cpp:115-151 + from_dense_edges :13-56):
