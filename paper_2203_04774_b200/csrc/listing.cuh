@@ -55,6 +55,7 @@ struct ListParams {
     const uint32_t* seeds;    // class list
     unsigned int nseeds;
     unsigned int* queue;      // dynamic work counter
+    const unsigned int* item_count;  // class G: number of {seed, part, parts} items in `seeds` (device)
     uint32_t* bitmaps;        // class G only: one n-bit bitmap per CTA
     uint64_t bitmap_words;
     uint32_t hot_rank;        // rows of ranks >= hot_rank (the most re-read ones) are loaded evict_last
@@ -367,6 +368,10 @@ struct Sink {
 constexpr uint32_t kLongRow = 96;  // rows at least this long are read in quad chunks
 constexpr uint32_t kSlotBytes = 512;  // one chunk (32 quads) in a shared-memory stage
 constexpr int kQU = 4;             // chunks per batch
+#ifndef TRIGPU_SHORT_W
+#define TRIGPU_SHORT_W 2  // (4: C3 -4 %, class R on C4 +3 %, per-vertex counts on C2 +8 %; 8: C3 +30 %)
+#endif
+constexpr int kShortW = TRIGPU_SHORT_W;  // 32-wide windows of the short-row stream per iteration
 
 struct Chunk {
     uint32_t qb;  // first quad (global quad index into out_adj)
@@ -683,37 +688,45 @@ __device__ __forceinline__ void scan_rows_at(const ListParams& P, uint32_t seed,
     const uint64_t rbase = cro - start;  // element f of the stream lives at out_adj[rbase(row) + f]
     const unsigned le = lanemask_le();
     int before = 0;
-    // two 32-wide windows per iteration: both loads are in flight before the
-    // first probe
-    for (uint32_t base = 0; base < total; base += 64) {
+    // kShortW 32-wide windows per iteration: all their loads are in flight
+    // before the first probe (a seed of short rows is latency-bound: the
+    // number of dependent round trips per seed is what it costs)
+    constexpr int W = Sink<ALGO, F>::kBuffered ? 2 : kShortW;
+    for (uint32_t base = 0; base < total; base += 32u * W) {
         const uint32_t rel = start - base;  // wraps when start < base: no bit
-        const unsigned bitA = (crl != 0 && start >= base && rel < 32u) ? (1u << rel) : 0u;
-        const unsigned bitB = (crl != 0 && start >= base && rel - 32u < 32u) ? (1u << (rel - 32u)) : 0u;
-        const unsigned MA = __reduce_or_sync(FULL, bitA);
-        const unsigned MB = __reduce_or_sync(FULL, bitB);
-        const int ca = __popc(MA);
-        int jA = before + __popc(MA & le) - 1;
-        int jB = before + ca + __popc(MB & le) - 1;
-        before += ca + __popc(MB);
-        jA = jA > 31 ? 31 : jA;
-        jB = jB > 31 ? 31 : jB;
-        const uint32_t fA = base + lane, fB = fA + 32;
-        const bool actA = fA < total, actB = fB < total;
-        const uint64_t rbA = shfl64(rbase, jA);
-        const uint64_t rbB = shfl64(rbase, jB);
-        const uint32_t yA = actA ? __ldg(P.out_adj + rbA + fA) : kNone;
-        const uint32_t yB = actB ? __ldg(P.out_adj + rbB + fB) : kNone;
-        const bool hitA = probe_one(probe, yA, actA);
-        const bool hitB = probe_one(probe, yB, actB);
-        hits += (unsigned)hitA + (unsigned)hitB;
-        if constexpr (F != 0u) {
-            const uint32_t xA = __shfl_sync(FULL, cx, jA), xB = __shfl_sync(FULL, cx, jB);
-            sink.direct(P, hitA, xA, yA);
-            sink.direct(P, hitB, xB, yB);
-            if constexpr (Sink<ALGO, F>::kBuffered) {
-                sink.batch(hitA, xA, yA);
-                sink.batch(hitB, xB, yB);
-                sink.drain(P, seed);
+        const bool own = crl != 0 && start >= base;
+        int j[W];
+        int acc = before;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            const uint32_t o = rel - 32u * w;
+            const unsigned M = __reduce_or_sync(FULL, (own && o < 32u) ? (1u << o) : 0u);
+            const int jj = acc + __popc(M & le) - 1;
+            j[w] = jj > 31 ? 31 : jj;
+            acc += __popc(M);
+        }
+        before = acc;
+        uint32_t y[W];
+        bool act[W];
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            const uint32_t f = base + 32u * w + lane;
+            act[w] = f < total;
+            const uint64_t rb = shfl64(rbase, j[w]);
+            y[w] = act[w] ? __ldg(P.out_adj + rb + f) : kNone;
+        }
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            if (w >= 2 && base + 32u * w >= total) break;  // uniform: no element in this window
+            const bool hit = probe_one(probe, y[w], act[w]);
+            hits += (unsigned)hit;
+            if constexpr (F != 0u) {
+                const uint32_t xw = __shfl_sync(FULL, cx, j[w]);
+                sink.direct(P, hit, xw, y[w]);
+                if constexpr (Sink<ALGO, F>::kBuffered) {
+                    sink.batch(hit, xw, y[w]);
+                    if (w & 1) sink.drain(P, seed);
+                }
             }
         }
     }
@@ -733,6 +746,9 @@ __device__ __forceinline__ void scan_rows(const ListParams& P, uint32_t seed, ui
 }
 
 // Chunks of 32 x's: set elements c, c + stride, ... below xe of the seed row at so.
+// (Loading the next chunk's x's and row offsets ahead of the current chunk's
+// streaming measured 2-3 % slower for class H on C4: the extra live registers
+// cost more than the two round trips per 32 rows.)
 template <int ALGO, unsigned F, class Probe>
 __device__ __forceinline__ void scan_x_range(const ListParams& P, uint32_t seed, uint64_t so, uint32_t cb,
                                              uint32_t xe, uint32_t stride, const Probe& probe, Sink<ALGO, F>& sink) {
@@ -1025,7 +1041,25 @@ struct CtaCfg {
 #ifndef TRIGPU_H_BITS_A_CTA
 #define TRIGPU_H_BITS_A_CTA 17
 #endif
-using CfgC1 = CtaCfg<256, TRIGPU_C1_BITS_A, 14, 1024, TRIGPU_C1_MINB, TRIGPU_C1_RING>;  // (2^17 window at 4 CTAs/SM: C4 -1 %, C5 +4 %)
+#ifndef TRIGPU_C1_THREADS
+#define TRIGPU_C1_THREADS 256
+#endif
+#ifndef TRIGPU_C1_PF
+#define TRIGPU_C1_RA 0  // 1: run-ahead kernel (k_list_cta_ra)
+#endif
+#ifndef TRIGPU_HW_RA
+#define TRIGPU_HW_RA 0
+#endif
+#ifndef TRIGPU_HW_BITS_A
+#define TRIGPU_HW_BITS_A 19
+#endif
+#ifndef TRIGPU_HW_THREADS
+#define TRIGPU_HW_THREADS 256
+#endif
+#ifndef TRIGPU_HW_MINB
+#define TRIGPU_HW_MINB 3
+#endif
+using CfgC1 = CtaCfg<TRIGPU_C1_THREADS, TRIGPU_C1_BITS_A, 14, 1024, TRIGPU_C1_MINB, TRIGPU_C1_RING>;  // (2^17 window at 4 CTAs/SM: C4 -1 %, C5 +4 %)
 #ifndef TRIGPU_C2_BITS_A
 #define TRIGPU_C2_BITS_A 19
 #endif
@@ -1035,7 +1069,7 @@ using CfgH = CtaCfg<256, TRIGPU_H_BITS_A_CTA, 13, 256, TRIGPU_H_MINB, TRIGPU_H_R
 // many ranks that the per-warp 2^16 window leaves many of its elements to the
 // filter + verification path; a CTA per seed shares one 2^19 window
 // (measured on C5: H 1275 -> 1147 ms; on C4 the warp kernel stays faster).
-using CfgHWide = CtaCfg<256, 19, 13, 256, 3, 0>;
+using CfgHWide = CtaCfg<TRIGPU_HW_THREADS, TRIGPU_HW_BITS_A, 13, 256, TRIGPU_HW_MINB, 0>;
 constexpr uint32_t kHWideMinN = 1u << 25;
 template <class CFG>
 constexpr size_t cta_bitmap_bytes() { return win_bytes(CFG::kBitsA, CFG::kBitsB); }
@@ -1198,6 +1232,156 @@ __global__ void __launch_bounds__(CFG::kThreads, CFG::kMinBlocks) k_list_cta(Lis
     flush_hist(P, sink);
 }
 
+// ---- class C / H-wide without CTA barriers (run-ahead) -------------------------
+// k_list_cta stops the whole CTA twice per seed (set-up, then the wait for the
+// seed's slowest warp): on C5 ~30 % of its stall samples sit at those barriers
+// (profiles/r02c_ncu_c5.md). Here the per-seed state is double-buffered -
+// two bitmaps, two row tables - and there is no CTA-wide barrier in the loop:
+//   * one producer warp prepares seed k + 1 in buffer (k + 1) & 1 (queue
+//     atomic, the set's x's, their row offsets / lengths, the chunk prefix,
+//     the bitmap bits) while the consumer warps stream seed k, then arrives on
+//     full[b] (mbarrier, count 1);
+//   * a consumer warp waits on full[b], streams its share of the seed's chunks
+//     and arrives on empty[b] (count = consumer warps); it goes on to the next
+//     seed at once, so a warp that finishes early runs ahead by up to one seed
+//     instead of idling at a barrier;
+//   * the producer waits on empty[b] before it clears bitmap b (from the old
+//     row table) and reuses the buffer.
+struct SeedMeta {  // one per buffer
+    uint32_t seed, d, nchunks, done;
+    uint32_t so_lo, so_hi, s0, top;
+};
+template <class CFG>
+constexpr size_t cta_ra_bytes() {
+    return 2 * cta_bitmap_bytes<CFG>() + 2 * cta_row_bytes<CFG>() + 2 * sizeof(SeedMeta) + 4 * 8;
+}
+
+template <int ALGO, unsigned F, class CFG>
+__global__ void __launch_bounds__(CFG::kThreads + 32, CFG::kMinBlocks) k_list_cta_ra(ListParams P) {
+    constexpr int kAll = CFG::kThreads + 32;  // consumer warps + the producer warp
+    constexpr uint32_t kWords = cta_bitmap_bytes<CFG>() / 4;
+    extern __shared__ __align__(16) unsigned char dsm[];
+    unsigned char* const bm0 = dsm + warp_scratch_bytes<F>(CFG::kWarps);
+    unsigned char* const tab0 = bm0 + 2 * cta_bitmap_bytes<CFG>();
+    SeedMeta* const metas = reinterpret_cast<SeedMeta*>(tab0 + 2 * cta_row_bytes<CFG>());
+    const unsigned bars = smem_addr(metas + 2);  // full[0], full[1], empty[0], empty[1]
+    for (uint32_t i = threadIdx.x; i < 2 * kWords; i += kAll) reinterpret_cast<uint32_t*>(bm0)[i] = 0u;
+    if (threadIdx.x == 0) {
+        mbar_init(bars + 0, 1);
+        mbar_init(bars + 8, 1);
+        mbar_init(bars + 16, CFG::kWarps);
+        mbar_init(bars + 24, CFG::kWarps);
+    }
+    Sink<ALGO, F> sink;
+    attach_scratch(sink, dsm);
+    __syncthreads();
+    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+    if (warp == (unsigned)CFG::kWarps) {
+        // ---- producer
+        for (unsigned k = 0;; ++k) {
+            const unsigned b = k & 1u;
+            SeedMeta* const mt = metas + b;
+            uint32_t* const bma = reinterpret_cast<uint32_t*>(bm0 + b * cta_bitmap_bytes<CFG>());
+            uint32_t* const bmb = bma + ((1u << CFG::kBitsA) / 32 + 4);
+            const unsigned rows = smem_addr(tab0 + b * cta_row_bytes<CFG>());
+            if (k >= 2) {
+                // every consumer warp is done with seed k - 2: clear its bits
+                mbar_wait(bars + 16 + 8 * b, ((k >> 1) - 1u) & 1u);
+                const WinGeom g0 = win_geom(CFG::kBitsA, CFG::kBitsB, P.bm_shrink, mt->s0, mt->top);
+                const uint32_t d0 = mt->d;
+                for (uint32_t i = lane; i < d0; i += 32) win_clear(bma, bmb, g0, lds32(rows + 16u * i + 12u));
+                __syncwarp();
+            }
+            unsigned u = 0;
+            if (lane == 0) u = atomicAdd(P.queue, 1u);
+            u = __shfl_sync(FULL, u, 0);
+            const bool done = u >= P.nseeds;
+            if (!done) {
+                const uint32_t seed = P.seeds[u];
+                const uint64_t so = P.set_off[seed];
+                const uint32_t d = P.set_len[seed];
+                const uint32_t* row = P.set_adj + so;
+                const uint32_t s0 = __ldg(row), top = __ldg(row + d - 1);
+                const WinGeom g = win_geom(CFG::kBitsA, CFG::kBitsB, P.bm_shrink, s0, top);
+                uint32_t run = 0;     // chunks before this group of set elements
+                constexpr int G = 8;  // groups of 32 set elements with their loads in flight together
+                for (uint32_t i0 = 0; i0 < d; i0 += 32u * G) {
+                    uint32_t x[G], q0[G], nq[G];
+#pragma unroll
+                    for (int g_ = 0; g_ < G; ++g_) {
+                        const uint32_t i = i0 + 32u * g_ + lane;
+                        x[g_] = i < d ? __ldg(row + i) : kNone;
+                    }
+#pragma unroll
+                    for (int g_ = 0; g_ < G; ++g_) {
+                        q0[g_] = 0;
+                        nq[g_] = 0;
+                        if (x[g_] != kNone) {
+                            q0[g_] = static_cast<uint32_t>(P.out_off[x[g_]] >> 2);
+                            nq[g_] = (P.out_len[x[g_]] + 3u) >> 2;
+                        }
+                    }
+#pragma unroll
+                    for (int g_ = 0; g_ < G; ++g_) {
+                        if (i0 + 32u * g_ >= d) break;
+                        const uint32_t i = i0 + 32u * g_ + lane;
+                        const uint32_t nc = row_chunks(nq[g_]);
+                        const uint32_t incl = warp_incl_scan(nc);
+                        if (i < d) {
+                            sts128(rows + 16u * i, make_uint4(q0[g_], nq[g_], run + incl - nc, x[g_]));
+                            win_set(bma, bmb, g, x[g_]);
+                        }
+                        run += __shfl_sync(FULL, incl, 31);
+                    }
+                }
+                if (lane == 0) {
+                    mt->seed = seed;
+                    mt->d = d;
+                    mt->nchunks = run;
+                    mt->so_lo = static_cast<uint32_t>(so);
+                    mt->so_hi = static_cast<uint32_t>(so >> 32);
+                    mt->s0 = s0;
+                    mt->top = top;
+                }
+            }
+            if (lane == 0) mt->done = done ? 1u : 0u;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bars + 8 * b);  // release: buffer b is ready
+            if (done) break;
+        }
+    } else {
+        // ---- consumers
+        for (unsigned k = 0;; ++k) {
+            const unsigned b = k & 1u;
+            mbar_wait(bars + 8 * b, (k >> 1) & 1u);
+            const SeedMeta mt = metas[b];
+            if (mt.done) break;
+            const unsigned bma = smem_addr(bm0 + b * cta_bitmap_bytes<CFG>());
+            const unsigned bmb = bma + ((1u << CFG::kBitsA) / 32 + 4) * 4u;
+            const unsigned rows = smem_addr(tab0 + b * cta_row_bytes<CFG>());
+            const uint32_t seed = mt.seed, d = mt.d, nchunks = mt.nchunks;
+            const uint64_t so = (static_cast<uint64_t>(mt.so_hi) << 32) | mt.so_lo;
+            const uint32_t gb = static_cast<uint32_t>((static_cast<uint64_t>(nchunks) * warp) / CFG::kWarps);
+            const uint32_t ge = static_cast<uint32_t>((static_cast<uint64_t>(nchunks) * (warp + 1)) / CFG::kWarps);
+            if (gb < ge) {
+                sink.begin_unit(P, seed);
+                const WinGeom g = win_geom(CFG::kBitsA, CFG::kBitsB, P.bm_shrink, mt.s0, mt.top);
+                with_win_probe(P, bma, bmb, g, RowVerify{P.set_adj + so, d}, [&](const auto& probe) {
+                    unsigned hits = 0;
+                    CtaRowCursor cur(rows, d, gb, ge);
+                    stream_quads<ALGO, F, false>(P, seed, cur, probe, sink, hits);
+                    sink.cnt += hits;
+                });
+                sink.end_unit(P, seed);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bars + 16 + 8 * b);  // this warp is done with buffer b
+        }
+    }
+    sink.flush(P);
+    flush_hist(P, sink);
+}
+
 // ---- class G: |S| > 4096, CTA per seed ---------------------------------------
 // A 2^20-rank shared-memory window over the set's top ranks (as the other
 // classes), and for the set's elements below the window an exact n-bit
@@ -1242,6 +1426,44 @@ struct WinGlobalProbe {
     __device__ __forceinline__ uint32_t sentinel() const { return kNone; }
 };
 
+// A giant seed is cut into `parts` work items, each a CTA's worth of the
+// seed's x chunks (interleaved, so the parts carry equal work): without the cut
+// one CTA would list a whole hub whose work is a large share of the class
+// (the tail of the launch). parts = work / max(kGItemWork, 16 |S|) - every part
+// rebuilds the seed's bitmaps, O(|S|) - and at most one part per 256 x's.
+constexpr unsigned long long kGItemWork = 1ull << 22;
+__global__ void __launch_bounds__(256) k_giant_items(const uint32_t* __restrict__ seeds, unsigned nseeds,
+                                                    const uint64_t* __restrict__ set_off,
+                                                    const uint32_t* __restrict__ set_len,
+                                                    const uint32_t* __restrict__ set_adj,
+                                                    const uint32_t* __restrict__ out_len, uint32_t* __restrict__ items,
+                                                    unsigned int* __restrict__ count, unsigned cap) {
+    const unsigned lane = lane_id();
+    const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; i < nseeds; i += warps) {
+        const uint32_t r = seeds[i];
+        const uint64_t so = set_off[r];
+        const uint32_t d = set_len[r];
+        unsigned long long w = 0;
+        for (uint32_t k = lane; k < d; k += 32) w += out_len[set_adj[so + k]];
+        w = warp_sum64(w);
+        const unsigned long long per = max(kGItemWork, 16ull * d);
+        unsigned long long np = (w + per - 1) / per;
+        np = min(np, (unsigned long long)((d + 255u) / 256u));
+        np = max(np, 1ull);
+        unsigned base = 0;
+        if (lane == 0) base = atomicAdd(count, (unsigned)np);
+        base = __shfl_sync(FULL, base, 0);
+        for (unsigned k = lane; k < (unsigned)np; k += 32) {
+            if (base + k < cap) {
+                items[3u * (base + k)] = r;
+                items[3u * (base + k) + 1] = k;
+                items[3u * (base + k) + 2] = (unsigned)np;
+            }
+        }
+    }
+}
+
 template <int ALGO, unsigned F>
 __global__ void __launch_bounds__(kGThreads) k_list_giant(ListParams P) {
     extern __shared__ __align__(16) unsigned char dsm[];
@@ -1259,8 +1481,9 @@ __global__ void __launch_bounds__(kGThreads) k_list_giant(ListParams P) {
         if (threadIdx.x == 0) unit = atomicAdd(P.queue, 1u);
         __syncthreads();
         const unsigned u = unit;
-        if (u >= P.nseeds) break;
-        const uint32_t seed = P.seeds[u];
+        if (u >= *P.item_count) break;
+        // one item = one of `parts` interleaved slices of a seed's x chunks
+        const uint32_t seed = P.seeds[3u * u], part = P.seeds[3u * u + 1], parts = P.seeds[3u * u + 2];
         sink.begin_unit(P, seed);
         const uint64_t so = P.set_off[seed];
         const uint32_t d = P.set_len[seed];
@@ -1281,7 +1504,7 @@ __global__ void __launch_bounds__(kGThreads) k_list_giant(ListParams P) {
         }
         __syncthreads();
         const WinGlobalProbe probe{smem_addr(win), wb, la, bm, smem_addr(coarse), cs};
-        scan_x_range<ALGO, F>(P, seed, so, warp * 32, d, kGWarps * 32, probe, sink);
+        scan_x_range<ALGO, F>(P, seed, so, (part * kGWarps + warp) * 32u, d, parts * kGWarps * 32u, probe, sink);
         sink.end_unit(P, seed);
         __syncthreads();
         for (uint32_t k = threadIdx.x; k < d; k += kGThreads) {
@@ -1302,6 +1525,7 @@ __global__ void __launch_bounds__(kGThreads) k_list_giant(ListParams P) {
 template <unsigned F> constexpr size_t smem_reg() { return warp_scratch_bytes<F>(kRWarps) + kRWarps * kRBmBytes; }
 template <unsigned F> constexpr size_t smem_warp() { return warp_scratch_bytes<F>(kHWarps) + kHWarps * kHBmBytes; }
 template <unsigned F, class CFG> constexpr size_t smem_cta() { return warp_scratch_bytes<F>(CFG::kWarps) + cta_bitmap_bytes<CFG>() + cta_row_bytes<CFG>() + cta_ring_bytes<CFG>(); }
+template <unsigned F, class CFG> constexpr size_t smem_cta_ra() { return warp_scratch_bytes<F>(CFG::kWarps) + cta_ra_bytes<CFG>(); }
 template <unsigned F> constexpr size_t smem_giant() { return warp_scratch_bytes<F>(kGWarps) + kGWinBytes + kGCoarseBytes; }
 
 // ---- seed classification --------------------------------------------------

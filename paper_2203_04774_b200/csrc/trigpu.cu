@@ -115,7 +115,7 @@ struct tl_ctx {
 
     DevBuf holes, segs;  // list compaction: chunk tails {start, len}; move segments
     DevBuf goff, gadj, rank, inv, hv, sort_tmp, labels, radj, out_off, out_adj, in_off, in_adj, outdeg, indeg, lists, acc,
-        vcount, tri, scan_part, bitmaps, small;
+        vcount, tri, scan_part, bitmaps, small, gitems;
     bool have_vcounts = false, have_tri = false;
     int variant = 0;         // TL_DEBUG_VARIANT: probe flavour of an experiments build (A/B timing)
     uint32_t bm_shrink = 0;  // TL_DEBUG_BM_SHRINK: smaller bitmaps (tests force the filter path)
@@ -489,6 +489,21 @@ tl_status launch_cta(tl_ctx* ctx, ListParams p, uint32_t* list, unsigned count, 
     return TL_OK;
 }
 
+template <int ALGO, unsigned F, class CFG>
+tl_status launch_cta_ra(tl_ctx* ctx, ListParams p, uint32_t* list, unsigned count, unsigned int* queue) {
+    p.seeds = list;
+    p.nseeds = count;
+    p.queue = queue;
+    const size_t smem = smem_cta_ra<F, CFG>();
+    tl_status st = set_smem(ctx, k_list_cta_ra<ALGO, F, CFG>, smem);
+    if (st != TL_OK) return st;
+    const unsigned grid =
+        std::min<unsigned>(count, resident_grid(ctx, k_list_cta_ra<ALGO, F, CFG>, CFG::kThreads + 32, smem));
+    k_list_cta_ra<ALGO, F, CFG><<<grid, CFG::kThreads + 32, smem, ctx->s>>>(p);
+    LAUNCHED();
+    return TL_OK;
+}
+
 template <int ALGO, unsigned F>
 tl_status launch_classes(tl_ctx* ctx, ListParams base, uint32_t* const lists[kClasses], const unsigned h[kClasses],
                          unsigned int* queues) {
@@ -496,15 +511,26 @@ tl_status launch_classes(tl_ctx* ctx, ListParams base, uint32_t* const lists[kCl
     // class G first, on the side stream: a few long CTAs overlap the rest
     if (h[4]) {
         ListParams p = base;
-        p.seeds = lists[4];
-        p.nseeds = h[4];
         p.queue = queues + 4;
+        // work items {seed, part, parts}: at most total work / kGItemWork + one per seed
+        const unsigned long long work = ALGO == ALGO_APM ? ctx->cost[1] : ctx->cost[0];
+        const unsigned long long cap64 = work / kGItemWork + h[4] + 16;
+        if (cap64 > 0x3FFFFFFFull) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "tl_list: too many class G work items");
+        const unsigned cap = static_cast<unsigned>(cap64);
+        ENSURE(gitems, (size_t)cap * 12);
+        k_giant_items<<<grid_for((uint64_t)h[4] * 32, 256, ctx->sms * 8), 256, 0, ctx->s>>>(
+            lists[4], h[4], base.set_off, base.set_len, base.set_adj, base.out_len, P<uint32_t>(ctx->gitems),
+            queues + 5, cap);
+        LAUNCHED();
+        p.seeds = P<uint32_t>(ctx->gitems);
+        p.nseeds = h[4];
+        p.item_count = queues + 5;
         const size_t smem = smem_giant<F>();
         if ((st = set_smem(ctx, k_list_giant<ALGO, F>, smem)) != TL_OK) return st;
 #ifndef TRIGPU_G_GRID
 #define TRIGPU_G_GRID 0  // CTAs for class G (0: one per SM)
 #endif
-        const unsigned grid = std::min<unsigned>(h[4], TRIGPU_G_GRID ? TRIGPU_G_GRID : (unsigned)ctx->sms);
+        const unsigned grid = TRIGPU_G_GRID ? TRIGPU_G_GRID : (unsigned)ctx->sms;  // items >= seeds; count is on the device
         p.bitmap_words = ((uint64_t)ctx->n + 31) / 32 + 32;
         const size_t bm_bytes = (size_t)grid * p.bitmap_words * 4;
         if (ctx->bitmaps.cap < bm_bytes) {
@@ -546,7 +572,11 @@ tl_status launch_classes(tl_ctx* ctx, ListParams base, uint32_t* const lists[kCl
 #else
       if (ctx->n > ctx->h_wide_min_n) {
         CK(cudaEventRecord(ctx->cls_ev[2], ctx->s));
+#if TRIGPU_HW_RA
+        st = launch_cta_ra<ALGO, F, CfgHWide>(ctx, base, lists[1], h[1], queues + 1);
+#else
         st = launch_cta<ALGO, F, CfgHWide>(ctx, base, lists[1], h[1], queues + 1);
+#endif
         if (st != TL_OK) return st;
         CK(cudaEventRecord(ctx->cls_ev[3], ctx->s));
       } else {
@@ -568,7 +598,11 @@ tl_status launch_classes(tl_ctx* ctx, ListParams base, uint32_t* const lists[kCl
     }
     if (h[2]) {
         CK(cudaEventRecord(ctx->cls_ev[4], ctx->s));
+#if TRIGPU_C1_RA
+        st = launch_cta_ra<ALGO, F, CfgC1>(ctx, base, lists[2], h[2], queues + 2);
+#else
         st = launch_cta<ALGO, F, CfgC1>(ctx, base, lists[2], h[2], queues + 2);
+#endif
         if (st != TL_OK) return st;
         CK(cudaEventRecord(ctx->cls_ev[5], ctx->s));
         ctx->cls_run[2] = true;
@@ -652,7 +686,7 @@ TL_API void tl_destroy(tl_ctx* ctx) {
     DevBuf* bufs[] = {&ctx->goff,   &ctx->gadj,   &ctx->rank,  &ctx->inv,    &ctx->radj,      &ctx->out_off,
                       &ctx->out_adj, &ctx->in_off, &ctx->in_adj, &ctx->outdeg, &ctx->indeg,     &ctx->lists,
                       &ctx->acc,    &ctx->vcount, &ctx->tri,   &ctx->scan_part, &ctx->bitmaps, &ctx->small,
-                      &ctx->hv,     &ctx->sort_tmp, &ctx->labels, &ctx->holes, &ctx->segs};
+                      &ctx->hv,     &ctx->sort_tmp, &ctx->labels, &ctx->holes, &ctx->segs, &ctx->gitems};
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     for (auto& ev : ctx->ev) cudaEventDestroy(ev);
