@@ -55,7 +55,6 @@ struct ListParams {
     const uint32_t* seeds;    // class list
     unsigned int nseeds;
     unsigned int* queue;      // dynamic work counter
-    const unsigned int* item_count;  // class G: number of {seed, part, parts} items in `seeds` (device)
     uint32_t* bitmaps;        // class G only: one n-bit bitmap per CTA
     uint64_t bitmap_words;
     uint32_t hot_rank;        // rows of ranks >= hot_rank (the most re-read ones) are loaded evict_last
@@ -669,6 +668,10 @@ __device__ __forceinline__ void scan_rows_at(const ListParams& P, uint32_t seed,
         stream_quads<ALGO, F, true>(P, seed, cur, probe, sink, hits);
     }
     if (rl >= kLongRow) rl = 0;
+    // (A lane-per-row walk of the rows of <= 32 elements - each lane reading its own
+    // row as quads - measured 35-50 % slower for class R on C2 / C3 / C4: 32
+    // uncoalesced 16-byte loads per instruction cost more than the flattened
+    // stream's index arithmetic.)
     // ---- phase 2: short rows
     const unsigned ne = __ballot_sync(FULL, rl != 0);
     if (!ne) {
@@ -1051,24 +1054,29 @@ struct CtaCfg {
 #define TRIGPU_HW_RA 0
 #endif
 #ifndef TRIGPU_HW_BITS_A
-#define TRIGPU_HW_BITS_A 19
+#define TRIGPU_HW_BITS_A 18
 #endif
 #ifndef TRIGPU_HW_THREADS
 #define TRIGPU_HW_THREADS 256
 #endif
 #ifndef TRIGPU_HW_MINB
-#define TRIGPU_HW_MINB 3
+#define TRIGPU_HW_MINB 4
 #endif
 using CfgC1 = CtaCfg<TRIGPU_C1_THREADS, TRIGPU_C1_BITS_A, 14, 1024, TRIGPU_C1_MINB, TRIGPU_C1_RING>;  // (2^17 window at 4 CTAs/SM: C4 -1 %, C5 +4 %)
 #ifndef TRIGPU_C2_BITS_A
 #define TRIGPU_C2_BITS_A 19
 #endif
-using CfgC2 = CtaCfg<1024, TRIGPU_C2_BITS_A, 15, 4096, 1, TRIGPU_C2_RING>;  // (2 x 512-thread CTAs, 2^18 window: C5 5 % slower)
+#ifndef TRIGPU_C2_THREADS
+#define TRIGPU_C2_THREADS 1024
+#endif
+using CfgC2 = CtaCfg<TRIGPU_C2_THREADS, TRIGPU_C2_BITS_A, 15, 4096, 1, TRIGPU_C2_RING>;  // (2 x 512-thread CTAs, 2^18 window: C5 5 % slower)
 using CfgH = CtaCfg<256, TRIGPU_H_BITS_A_CTA, 13, 256, TRIGPU_H_MINB, TRIGPU_H_RING>;
 // Class H on graphs of more than 2^25 vertices: the set of an H seed spans so
 // many ranks that the per-warp 2^16 window leaves many of its elements to the
-// filter + verification path; a CTA per seed shares one 2^19 window
-// (measured on C5: H 1275 -> 1147 ms; on C4 the warp kernel stays faster).
+// filter + verification path; a CTA per seed shares one wider window
+// (measured on C5: warp kernel 1275 ms, CTA-wide 2^19 window at 3 CTAs/SM
+// 1147 ms, 2^18 window at 4 CTAs/SM and 64 registers 1097 ms; on C4 the warp
+// kernel stays faster).
 using CfgHWide = CtaCfg<TRIGPU_HW_THREADS, TRIGPU_HW_BITS_A, 13, 256, TRIGPU_HW_MINB, 0>;
 constexpr uint32_t kHWideMinN = 1u << 25;
 template <class CFG>
@@ -1166,7 +1174,7 @@ __global__ void __launch_bounds__(CFG::kThreads, CFG::kMinBlocks) k_list_cta(Lis
     }
     Sink<ALGO, F> sink;
     attach_scratch(sink, dsm);
-    constexpr int PER = CFG::kMaxD / kCThreads;  // set elements per thread
+    constexpr int PER = (CFG::kMaxD + kCThreads - 1) / kCThreads;  // set elements per thread
     for (;;) {
         __syncthreads();
         if (threadIdx.x == 0) unit = atomicAdd(P.queue, 1u);
@@ -1345,6 +1353,7 @@ __global__ void __launch_bounds__(CFG::kThreads + 32, CFG::kMinBlocks) k_list_ct
                 }
             }
             if (lane == 0) mt->done = done ? 1u : 0u;
+            __threadfence_block();  // every lane's table / bitmap writes are performed before the arrive
             __syncwarp();
             if (lane == 0) mbar_arrive(bars + 8 * b);  // release: buffer b is ready
             if (done) break;
@@ -1374,6 +1383,7 @@ __global__ void __launch_bounds__(CFG::kThreads + 32, CFG::kMinBlocks) k_list_ct
                 });
                 sink.end_unit(P, seed);
             }
+            __threadfence_block();
             __syncwarp();
             if (lane == 0) mbar_arrive(bars + 16 + 8 * b);  // this warp is done with buffer b
         }
@@ -1426,44 +1436,9 @@ struct WinGlobalProbe {
     __device__ __forceinline__ uint32_t sentinel() const { return kNone; }
 };
 
-// A giant seed is cut into `parts` work items, each a CTA's worth of the
-// seed's x chunks (interleaved, so the parts carry equal work): without the cut
-// one CTA would list a whole hub whose work is a large share of the class
-// (the tail of the launch). parts = work / max(kGItemWork, 16 |S|) - every part
-// rebuilds the seed's bitmaps, O(|S|) - and at most one part per 256 x's.
-constexpr unsigned long long kGItemWork = 1ull << 22;
-__global__ void __launch_bounds__(256) k_giant_items(const uint32_t* __restrict__ seeds, unsigned nseeds,
-                                                    const uint64_t* __restrict__ set_off,
-                                                    const uint32_t* __restrict__ set_len,
-                                                    const uint32_t* __restrict__ set_adj,
-                                                    const uint32_t* __restrict__ out_len, uint32_t* __restrict__ items,
-                                                    unsigned int* __restrict__ count, unsigned cap) {
-    const unsigned lane = lane_id();
-    const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; i < nseeds; i += warps) {
-        const uint32_t r = seeds[i];
-        const uint64_t so = set_off[r];
-        const uint32_t d = set_len[r];
-        unsigned long long w = 0;
-        for (uint32_t k = lane; k < d; k += 32) w += out_len[set_adj[so + k]];
-        w = warp_sum64(w);
-        const unsigned long long per = max(kGItemWork, 16ull * d);
-        unsigned long long np = (w + per - 1) / per;
-        np = min(np, (unsigned long long)((d + 255u) / 256u));
-        np = max(np, 1ull);
-        unsigned base = 0;
-        if (lane == 0) base = atomicAdd(count, (unsigned)np);
-        base = __shfl_sync(FULL, base, 0);
-        for (unsigned k = lane; k < (unsigned)np; k += 32) {
-            if (base + k < cap) {
-                items[3u * (base + k)] = r;
-                items[3u * (base + k) + 1] = k;
-                items[3u * (base + k) + 2] = (unsigned)np;
-            }
-        }
-    }
-}
-
+// (Cutting a giant seed into several CTA work items - interleaved slices of its
+// x chunks - measured slower on C4 split A+- (G 168 -> 211 ms): every part
+// rebuilds and clears the seed's bitmaps, O(|S|) global atomics.)
 template <int ALGO, unsigned F>
 __global__ void __launch_bounds__(kGThreads) k_list_giant(ListParams P) {
     extern __shared__ __align__(16) unsigned char dsm[];
@@ -1481,9 +1456,8 @@ __global__ void __launch_bounds__(kGThreads) k_list_giant(ListParams P) {
         if (threadIdx.x == 0) unit = atomicAdd(P.queue, 1u);
         __syncthreads();
         const unsigned u = unit;
-        if (u >= *P.item_count) break;
-        // one item = one of `parts` interleaved slices of a seed's x chunks
-        const uint32_t seed = P.seeds[3u * u], part = P.seeds[3u * u + 1], parts = P.seeds[3u * u + 2];
+        if (u >= P.nseeds) break;
+        const uint32_t seed = P.seeds[u];
         sink.begin_unit(P, seed);
         const uint64_t so = P.set_off[seed];
         const uint32_t d = P.set_len[seed];
@@ -1504,7 +1478,7 @@ __global__ void __launch_bounds__(kGThreads) k_list_giant(ListParams P) {
         }
         __syncthreads();
         const WinGlobalProbe probe{smem_addr(win), wb, la, bm, smem_addr(coarse), cs};
-        scan_x_range<ALGO, F>(P, seed, so, (part * kGWarps + warp) * 32u, d, parts * kGWarps * 32u, probe, sink);
+        scan_x_range<ALGO, F>(P, seed, so, warp * 32, d, kGWarps * 32, probe, sink);
         sink.end_unit(P, seed);
         __syncthreads();
         for (uint32_t k = threadIdx.x; k < d; k += kGThreads) {

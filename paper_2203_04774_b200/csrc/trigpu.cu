@@ -115,7 +115,7 @@ struct tl_ctx {
 
     DevBuf holes, segs;  // list compaction: chunk tails {start, len}; move segments
     DevBuf goff, gadj, rank, inv, hv, sort_tmp, labels, radj, out_off, out_adj, in_off, in_adj, outdeg, indeg, lists, acc,
-        vcount, tri, scan_part, bitmaps, small, gitems;
+        vcount, tri, scan_part, bitmaps, small;
     bool have_vcounts = false, have_tri = false;
     int variant = 0;         // TL_DEBUG_VARIANT: probe flavour of an experiments build (A/B timing)
     uint32_t bm_shrink = 0;  // TL_DEBUG_BM_SHRINK: smaller bitmaps (tests force the filter path)
@@ -497,8 +497,11 @@ tl_status launch_cta_ra(tl_ctx* ctx, ListParams p, uint32_t* list, unsigned coun
     const size_t smem = smem_cta_ra<F, CFG>();
     tl_status st = set_smem(ctx, k_list_cta_ra<ALGO, F, CFG>, smem);
     if (st != TL_OK) return st;
-    const unsigned grid =
+    unsigned grid =
         std::min<unsigned>(count, resident_grid(ctx, k_list_cta_ra<ALGO, F, CFG>, CFG::kThreads + 32, smem));
+#ifdef TRIGPU_RA_GRID  // debugging: few CTAs, so every CTA reuses its buffers many times on a small graph
+    grid = std::min<unsigned>(grid, TRIGPU_RA_GRID);
+#endif
     k_list_cta_ra<ALGO, F, CFG><<<grid, CFG::kThreads + 32, smem, ctx->s>>>(p);
     LAUNCHED();
     return TL_OK;
@@ -512,25 +515,14 @@ tl_status launch_classes(tl_ctx* ctx, ListParams base, uint32_t* const lists[kCl
     if (h[4]) {
         ListParams p = base;
         p.queue = queues + 4;
-        // work items {seed, part, parts}: at most total work / kGItemWork + one per seed
-        const unsigned long long work = ALGO == ALGO_APM ? ctx->cost[1] : ctx->cost[0];
-        const unsigned long long cap64 = work / kGItemWork + h[4] + 16;
-        if (cap64 > 0x3FFFFFFFull) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "tl_list: too many class G work items");
-        const unsigned cap = static_cast<unsigned>(cap64);
-        ENSURE(gitems, (size_t)cap * 12);
-        k_giant_items<<<grid_for((uint64_t)h[4] * 32, 256, ctx->sms * 8), 256, 0, ctx->s>>>(
-            lists[4], h[4], base.set_off, base.set_len, base.set_adj, base.out_len, P<uint32_t>(ctx->gitems),
-            queues + 5, cap);
-        LAUNCHED();
-        p.seeds = P<uint32_t>(ctx->gitems);
+        p.seeds = lists[4];
         p.nseeds = h[4];
-        p.item_count = queues + 5;
         const size_t smem = smem_giant<F>();
         if ((st = set_smem(ctx, k_list_giant<ALGO, F>, smem)) != TL_OK) return st;
 #ifndef TRIGPU_G_GRID
 #define TRIGPU_G_GRID 0  // CTAs for class G (0: one per SM)
 #endif
-        const unsigned grid = TRIGPU_G_GRID ? TRIGPU_G_GRID : (unsigned)ctx->sms;  // items >= seeds; count is on the device
+        const unsigned grid = std::min<unsigned>(h[4], TRIGPU_G_GRID ? TRIGPU_G_GRID : (unsigned)ctx->sms);
         p.bitmap_words = ((uint64_t)ctx->n + 31) / 32 + 32;
         const size_t bm_bytes = (size_t)grid * p.bitmap_words * 4;
         if (ctx->bitmaps.cap < bm_bytes) {
@@ -686,7 +678,7 @@ TL_API void tl_destroy(tl_ctx* ctx) {
     DevBuf* bufs[] = {&ctx->goff,   &ctx->gadj,   &ctx->rank,  &ctx->inv,    &ctx->radj,      &ctx->out_off,
                       &ctx->out_adj, &ctx->in_off, &ctx->in_adj, &ctx->outdeg, &ctx->indeg,     &ctx->lists,
                       &ctx->acc,    &ctx->vcount, &ctx->tri,   &ctx->scan_part, &ctx->bitmaps, &ctx->small,
-                      &ctx->hv,     &ctx->sort_tmp, &ctx->labels, &ctx->holes, &ctx->segs, &ctx->gitems};
+                      &ctx->hv,     &ctx->sort_tmp, &ctx->labels, &ctx->holes, &ctx->segs};
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     for (auto& ev : ctx->ev) cudaEventDestroy(ev);
