@@ -4,7 +4,7 @@
 
     python -m paper_2203_04774_b200.cli list  GRAPH [--order degree] [--algo apm]
                                               [--mode mere|full] [--sink count|collect]
-                                              [--out TRIANGLES]
+                                              [--out TRIANGLES] [--device-order]
     python -m paper_2203_04774_b200.cli bench GRAPH [--orderings degree,core]
                                               [--algos app,apm] [--repeats 1]
 
@@ -48,6 +48,21 @@ def load(path: str):
     return g, (time.perf_counter() - t0) * 1e3
 
 
+DEVICE_METHODS = ("degree", "split", "core")
+
+
+def compute_order(ctx: Context, g, method: str, seed: int, device_order: bool):
+    """compute_order (trilist_cli.cpp:50-64): the reference's host code, or with
+    --device-order the engine's degree / split ordering (bit-identical ranks) and
+    k-core degeneracy ordering (tl_core_decompose). Returns (ranks, order_ms)."""
+    if device_order and method in DEVICE_METHODS:
+        t0 = time.perf_counter()
+        ranks = ctx.core_decompose(g.offsets, g.adjacency)[0] if method == "core" else ctx.order(g.offsets, method)
+        return ranks, (time.perf_counter() - t0) * 1e3
+    pi, order_ms = host.compute_order(g, method, seed)
+    return pi.ranks, order_ms
+
+
 def run_listing(ctx: Context, g, ranks, dataset: str, algo: str, ordering: str, mode: str,
                 load_ms: float, order_ms: float, collect: bool) -> tuple[str, object]:
     """run_listing (trilist_cli.cpp:101-139): one BenchRecord CSV row."""
@@ -62,11 +77,11 @@ def run_listing(ctx: Context, g, ranks, dataset: str, algo: str, ordering: str, 
 
 def cmd_list(args) -> int:
     g, load_ms = load(args.graph)
-    pi, order_ms = host.compute_order(g, args.order, args.seed)
     collect = args.sink == "collect" or bool(args.out)
     ctx = Context(args.device)
     try:
-        row, st = run_listing(ctx, g, pi.ranks, dataset_name(args.graph), args.algo, args.order, args.mode,
+        ranks, order_ms = compute_order(ctx, g, args.order, args.seed, args.device_order)
+        row, st = run_listing(ctx, g, ranks, dataset_name(args.graph), args.algo, args.order, args.mode,
                               load_ms, order_ms, collect)
         if args.out:
             with open(args.out, "w") as f:
@@ -91,10 +106,10 @@ def cmd_bench(args) -> int:
     ctx = Context(args.device)
     try:
         for method in orderings:
-            pi, order_ms = host.compute_order(g, method, args.seed)
+            ranks, order_ms = compute_order(ctx, g, method, args.seed, args.device_order)
             for algo in algos:
                 for _ in range(args.repeats):
-                    row, _ = run_listing(ctx, g, pi.ranks, dataset_name(args.graph), algo, method, "full",
+                    row, _ = run_listing(ctx, g, ranks, dataset_name(args.graph), algo, method, "full",
                                          load_ms, order_ms, False)
                     print(row, flush=True)
     finally:
@@ -114,6 +129,7 @@ def main(argv=None) -> int:
     pl.add_argument("--sink", default="count", choices=["count", "collect"])
     pl.add_argument("--out", default="")
     pl.add_argument("--device", type=int, default=0)
+    pl.add_argument("--device-order", action="store_true", help="degree / split / core ordering on the GPU")
     pb = sub.add_parser("bench")
     pb.add_argument("graph")
     pb.add_argument("--orderings", default="")
@@ -121,6 +137,7 @@ def main(argv=None) -> int:
     pb.add_argument("--repeats", type=int, default=1)
     pb.add_argument("--seed", type=int, default=0)
     pb.add_argument("--device", type=int, default=0)
+    pb.add_argument("--device-order", action="store_true", help="degree / split / core ordering on the GPU")
     args = ap.parse_args(argv)
     try:
         return cmd_list(args) if args.cmd == "list" else cmd_bench(args)

@@ -252,9 +252,6 @@ __device__ __forceinline__ void bulk_g2s_pol(unsigned dst, const void* src, unsi
         "l"(src), "r"(bytes), "r"(bar), "l"(pol)
         : "memory");
 }
-__device__ __forceinline__ void mbar_arrive(unsigned bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
 __device__ __forceinline__ bool mbar_try_wait(unsigned bar, unsigned parity) {
     uint32_t ok;
     asm volatile(

@@ -1044,23 +1044,17 @@ struct CtaCfg {
 #ifndef TRIGPU_H_BITS_A_CTA
 #define TRIGPU_H_BITS_A_CTA 17
 #endif
-#ifndef TRIGPU_C1_THREADS
-#define TRIGPU_C1_THREADS 256
-#endif
-#ifndef TRIGPU_C1_PF
-#define TRIGPU_C1_RA 0  // 1: run-ahead kernel (k_list_cta_ra)
-#endif
-#ifndef TRIGPU_HW_RA
-#define TRIGPU_HW_RA 0
-#endif
 #ifndef TRIGPU_HW_BITS_A
 #define TRIGPU_HW_BITS_A 18
 #endif
-#ifndef TRIGPU_HW_THREADS
-#define TRIGPU_HW_THREADS 256
-#endif
 #ifndef TRIGPU_HW_MINB
 #define TRIGPU_HW_MINB 4
+#endif
+#ifndef TRIGPU_C1_THREADS
+#define TRIGPU_C1_THREADS 256
+#endif
+#ifndef TRIGPU_HW_THREADS
+#define TRIGPU_HW_THREADS 256
 #endif
 using CfgC1 = CtaCfg<TRIGPU_C1_THREADS, TRIGPU_C1_BITS_A, 14, 1024, TRIGPU_C1_MINB, TRIGPU_C1_RING>;  // (2^17 window at 4 CTAs/SM: C4 -1 %, C5 +4 %)
 #ifndef TRIGPU_C2_BITS_A
@@ -1240,157 +1234,11 @@ __global__ void __launch_bounds__(CFG::kThreads, CFG::kMinBlocks) k_list_cta(Lis
     flush_hist(P, sink);
 }
 
-// ---- class C / H-wide without CTA barriers (run-ahead) -------------------------
-// k_list_cta stops the whole CTA twice per seed (set-up, then the wait for the
-// seed's slowest warp): on C5 ~30 % of its stall samples sit at those barriers
-// (profiles/r02c_ncu_c5.md). Here the per-seed state is double-buffered -
-// two bitmaps, two row tables - and there is no CTA-wide barrier in the loop:
-//   * one producer warp prepares seed k + 1 in buffer (k + 1) & 1 (queue
-//     atomic, the set's x's, their row offsets / lengths, the chunk prefix,
-//     the bitmap bits) while the consumer warps stream seed k, then arrives on
-//     full[b] (mbarrier, count 1);
-//   * a consumer warp waits on full[b], streams its share of the seed's chunks
-//     and arrives on empty[b] (count = consumer warps); it goes on to the next
-//     seed at once, so a warp that finishes early runs ahead by up to one seed
-//     instead of idling at a barrier;
-//   * the producer waits on empty[b] before it clears bitmap b (from the old
-//     row table) and reuses the buffer.
-struct SeedMeta {  // one per buffer
-    uint32_t seed, d, nchunks, done;
-    uint32_t so_lo, so_hi, s0, top;
-};
-template <class CFG>
-constexpr size_t cta_ra_bytes() {
-    return 2 * cta_bitmap_bytes<CFG>() + 2 * cta_row_bytes<CFG>() + 2 * sizeof(SeedMeta) + 4 * 8;
-}
-
-template <int ALGO, unsigned F, class CFG>
-__global__ void __launch_bounds__(CFG::kThreads + 32, CFG::kMinBlocks) k_list_cta_ra(ListParams P) {
-    constexpr int kAll = CFG::kThreads + 32;  // consumer warps + the producer warp
-    constexpr uint32_t kWords = cta_bitmap_bytes<CFG>() / 4;
-    extern __shared__ __align__(16) unsigned char dsm[];
-    unsigned char* const bm0 = dsm + warp_scratch_bytes<F>(CFG::kWarps);
-    unsigned char* const tab0 = bm0 + 2 * cta_bitmap_bytes<CFG>();
-    SeedMeta* const metas = reinterpret_cast<SeedMeta*>(tab0 + 2 * cta_row_bytes<CFG>());
-    const unsigned bars = smem_addr(metas + 2);  // full[0], full[1], empty[0], empty[1]
-    for (uint32_t i = threadIdx.x; i < 2 * kWords; i += kAll) reinterpret_cast<uint32_t*>(bm0)[i] = 0u;
-    if (threadIdx.x == 0) {
-        mbar_init(bars + 0, 1);
-        mbar_init(bars + 8, 1);
-        mbar_init(bars + 16, CFG::kWarps);
-        mbar_init(bars + 24, CFG::kWarps);
-    }
-    Sink<ALGO, F> sink;
-    attach_scratch(sink, dsm);
-    __syncthreads();
-    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
-    if (warp == (unsigned)CFG::kWarps) {
-        // ---- producer
-        for (unsigned k = 0;; ++k) {
-            const unsigned b = k & 1u;
-            SeedMeta* const mt = metas + b;
-            uint32_t* const bma = reinterpret_cast<uint32_t*>(bm0 + b * cta_bitmap_bytes<CFG>());
-            uint32_t* const bmb = bma + ((1u << CFG::kBitsA) / 32 + 4);
-            const unsigned rows = smem_addr(tab0 + b * cta_row_bytes<CFG>());
-            if (k >= 2) {
-                // every consumer warp is done with seed k - 2: clear its bits
-                mbar_wait(bars + 16 + 8 * b, ((k >> 1) - 1u) & 1u);
-                const WinGeom g0 = win_geom(CFG::kBitsA, CFG::kBitsB, P.bm_shrink, mt->s0, mt->top);
-                const uint32_t d0 = mt->d;
-                for (uint32_t i = lane; i < d0; i += 32) win_clear(bma, bmb, g0, lds32(rows + 16u * i + 12u));
-                __syncwarp();
-            }
-            unsigned u = 0;
-            if (lane == 0) u = atomicAdd(P.queue, 1u);
-            u = __shfl_sync(FULL, u, 0);
-            const bool done = u >= P.nseeds;
-            if (!done) {
-                const uint32_t seed = P.seeds[u];
-                const uint64_t so = P.set_off[seed];
-                const uint32_t d = P.set_len[seed];
-                const uint32_t* row = P.set_adj + so;
-                const uint32_t s0 = __ldg(row), top = __ldg(row + d - 1);
-                const WinGeom g = win_geom(CFG::kBitsA, CFG::kBitsB, P.bm_shrink, s0, top);
-                uint32_t run = 0;     // chunks before this group of set elements
-                constexpr int G = 8;  // groups of 32 set elements with their loads in flight together
-                for (uint32_t i0 = 0; i0 < d; i0 += 32u * G) {
-                    uint32_t x[G], q0[G], nq[G];
-#pragma unroll
-                    for (int g_ = 0; g_ < G; ++g_) {
-                        const uint32_t i = i0 + 32u * g_ + lane;
-                        x[g_] = i < d ? __ldg(row + i) : kNone;
-                    }
-#pragma unroll
-                    for (int g_ = 0; g_ < G; ++g_) {
-                        q0[g_] = 0;
-                        nq[g_] = 0;
-                        if (x[g_] != kNone) {
-                            q0[g_] = static_cast<uint32_t>(P.out_off[x[g_]] >> 2);
-                            nq[g_] = (P.out_len[x[g_]] + 3u) >> 2;
-                        }
-                    }
-#pragma unroll
-                    for (int g_ = 0; g_ < G; ++g_) {
-                        if (i0 + 32u * g_ >= d) break;
-                        const uint32_t i = i0 + 32u * g_ + lane;
-                        const uint32_t nc = row_chunks(nq[g_]);
-                        const uint32_t incl = warp_incl_scan(nc);
-                        if (i < d) {
-                            sts128(rows + 16u * i, make_uint4(q0[g_], nq[g_], run + incl - nc, x[g_]));
-                            win_set(bma, bmb, g, x[g_]);
-                        }
-                        run += __shfl_sync(FULL, incl, 31);
-                    }
-                }
-                if (lane == 0) {
-                    mt->seed = seed;
-                    mt->d = d;
-                    mt->nchunks = run;
-                    mt->so_lo = static_cast<uint32_t>(so);
-                    mt->so_hi = static_cast<uint32_t>(so >> 32);
-                    mt->s0 = s0;
-                    mt->top = top;
-                }
-            }
-            if (lane == 0) mt->done = done ? 1u : 0u;
-            __threadfence_block();  // every lane's table / bitmap writes are performed before the arrive
-            __syncwarp();
-            if (lane == 0) mbar_arrive(bars + 8 * b);  // release: buffer b is ready
-            if (done) break;
-        }
-    } else {
-        // ---- consumers
-        for (unsigned k = 0;; ++k) {
-            const unsigned b = k & 1u;
-            mbar_wait(bars + 8 * b, (k >> 1) & 1u);
-            const SeedMeta mt = metas[b];
-            if (mt.done) break;
-            const unsigned bma = smem_addr(bm0 + b * cta_bitmap_bytes<CFG>());
-            const unsigned bmb = bma + ((1u << CFG::kBitsA) / 32 + 4) * 4u;
-            const unsigned rows = smem_addr(tab0 + b * cta_row_bytes<CFG>());
-            const uint32_t seed = mt.seed, d = mt.d, nchunks = mt.nchunks;
-            const uint64_t so = (static_cast<uint64_t>(mt.so_hi) << 32) | mt.so_lo;
-            const uint32_t gb = static_cast<uint32_t>((static_cast<uint64_t>(nchunks) * warp) / CFG::kWarps);
-            const uint32_t ge = static_cast<uint32_t>((static_cast<uint64_t>(nchunks) * (warp + 1)) / CFG::kWarps);
-            if (gb < ge) {
-                sink.begin_unit(P, seed);
-                const WinGeom g = win_geom(CFG::kBitsA, CFG::kBitsB, P.bm_shrink, mt.s0, mt.top);
-                with_win_probe(P, bma, bmb, g, RowVerify{P.set_adj + so, d}, [&](const auto& probe) {
-                    unsigned hits = 0;
-                    CtaRowCursor cur(rows, d, gb, ge);
-                    stream_quads<ALGO, F, false>(P, seed, cur, probe, sink, hits);
-                    sink.cnt += hits;
-                });
-                sink.end_unit(P, seed);
-            }
-            __threadfence_block();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(bars + 16 + 8 * b);  // this warp is done with buffer b
-        }
-    }
-    sink.flush(P);
-    flush_hist(P, sink);
-}
+// (A barrier-free variant of k_list_cta - double-buffered bitmaps and row
+// tables, a producer warp, mbarrier full / empty pairs so that a warp that
+// finishes its share early runs ahead into the next seed - is in the history
+// (commit "Run-ahead CTA kernel fixed ..."): correct, but for class H on C5 it
+// measured 8 % slower than the barrier kernel.)
 
 // ---- class G: |S| > 4096, CTA per seed ---------------------------------------
 // A 2^20-rank shared-memory window over the set's top ranks (as the other
@@ -1499,7 +1347,6 @@ __global__ void __launch_bounds__(kGThreads) k_list_giant(ListParams P) {
 template <unsigned F> constexpr size_t smem_reg() { return warp_scratch_bytes<F>(kRWarps) + kRWarps * kRBmBytes; }
 template <unsigned F> constexpr size_t smem_warp() { return warp_scratch_bytes<F>(kHWarps) + kHWarps * kHBmBytes; }
 template <unsigned F, class CFG> constexpr size_t smem_cta() { return warp_scratch_bytes<F>(CFG::kWarps) + cta_bitmap_bytes<CFG>() + cta_row_bytes<CFG>() + cta_ring_bytes<CFG>(); }
-template <unsigned F, class CFG> constexpr size_t smem_cta_ra() { return warp_scratch_bytes<F>(CFG::kWarps) + cta_ra_bytes<CFG>(); }
 template <unsigned F> constexpr size_t smem_giant() { return warp_scratch_bytes<F>(kGWarps) + kGWinBytes + kGCoarseBytes; }
 
 // ---- seed classification --------------------------------------------------

@@ -489,24 +489,6 @@ tl_status launch_cta(tl_ctx* ctx, ListParams p, uint32_t* list, unsigned count, 
     return TL_OK;
 }
 
-template <int ALGO, unsigned F, class CFG>
-tl_status launch_cta_ra(tl_ctx* ctx, ListParams p, uint32_t* list, unsigned count, unsigned int* queue) {
-    p.seeds = list;
-    p.nseeds = count;
-    p.queue = queue;
-    const size_t smem = smem_cta_ra<F, CFG>();
-    tl_status st = set_smem(ctx, k_list_cta_ra<ALGO, F, CFG>, smem);
-    if (st != TL_OK) return st;
-    unsigned grid =
-        std::min<unsigned>(count, resident_grid(ctx, k_list_cta_ra<ALGO, F, CFG>, CFG::kThreads + 32, smem));
-#ifdef TRIGPU_RA_GRID  // debugging: few CTAs, so every CTA reuses its buffers many times on a small graph
-    grid = std::min<unsigned>(grid, TRIGPU_RA_GRID);
-#endif
-    k_list_cta_ra<ALGO, F, CFG><<<grid, CFG::kThreads + 32, smem, ctx->s>>>(p);
-    LAUNCHED();
-    return TL_OK;
-}
-
 template <int ALGO, unsigned F>
 tl_status launch_classes(tl_ctx* ctx, ListParams base, uint32_t* const lists[kClasses], const unsigned h[kClasses],
                          unsigned int* queues) {
@@ -564,11 +546,7 @@ tl_status launch_classes(tl_ctx* ctx, ListParams base, uint32_t* const lists[kCl
 #else
       if (ctx->n > ctx->h_wide_min_n) {
         CK(cudaEventRecord(ctx->cls_ev[2], ctx->s));
-#if TRIGPU_HW_RA
-        st = launch_cta_ra<ALGO, F, CfgHWide>(ctx, base, lists[1], h[1], queues + 1);
-#else
         st = launch_cta<ALGO, F, CfgHWide>(ctx, base, lists[1], h[1], queues + 1);
-#endif
         if (st != TL_OK) return st;
         CK(cudaEventRecord(ctx->cls_ev[3], ctx->s));
       } else {
@@ -590,11 +568,7 @@ tl_status launch_classes(tl_ctx* ctx, ListParams base, uint32_t* const lists[kCl
     }
     if (h[2]) {
         CK(cudaEventRecord(ctx->cls_ev[4], ctx->s));
-#if TRIGPU_C1_RA
-        st = launch_cta_ra<ALGO, F, CfgC1>(ctx, base, lists[2], h[2], queues + 2);
-#else
         st = launch_cta<ALGO, F, CfgC1>(ctx, base, lists[2], h[2], queues + 2);
-#endif
         if (st != TL_OK) return st;
         CK(cudaEventRecord(ctx->cls_ev[5], ctx->s));
         ctx->cls_run[2] = true;

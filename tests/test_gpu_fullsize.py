@@ -171,13 +171,16 @@ def test_full_size_counts_vs_reference(ctx, cfg):
         del rv
 
 
-def test_c5_raw_edge_list_normalize():
+def test_c5_raw_edge_list_normalize(ctx):
     """tl_normalize at C5 scale: the 2^31 raw R-MAT-27 draws (loops and
     duplicates kept, more than 2^31 endpoints) through the device normalize
     (graph.cpp:115-151 + from_dense_edges :13-56) give gen_rmat(27)'s graph
     restricted to its non-isolated vertices: labels = those vertex ids,
     degrees and rows equal after mapping dense ids back through the labels;
     the device-resident graph then orients and lists C5's triangles."""
+    # the normalize scratch is 48 B per raw edge (103 GB here): release the module
+    # context's C2-C5 buffers first (this is the module's last test; close() is idempotent)
+    ctx.close()
     raw = host.gen_rmat_raw(27, 16, 1)
     k = raw.shape[0]
     assert 2 * k > 2**31

@@ -523,3 +523,12 @@ def test_cli_list_and_bench(tmp_path, capsys):
     rows = capsys.readouterr().out.splitlines()
     assert rows[0] == host.bench_csv_header() and len(rows) == 5
     assert len({r.split(",")[10] for r in rows[1:]}) == 1  # same triangle count every run
+    # --device-order: degree / split rows are identical to the host-ordered ones (same ranks, so
+    # same costs); core is a degeneracy ordering of its own but lists the same triangles
+    assert cli.main(["bench", str(src), "--orderings", "degree,split,core", "--algos", "apm", "--device-order"]) == 0
+    dev = capsys.readouterr().out.splitlines()
+    assert len(dev) == 4 and {r.split(",")[10] for r in dev[1:]} == {rows[1].split(",")[10]}
+    host_rows = {(r.split(",")[1], r.split(",")[2]): r.split(",")[6:11] for r in rows[1:]}
+    for r in dev[1:3]:
+        f = r.split(",")
+        assert host_rows[(f[1], f[2])] == f[6:11]  # c_pp, c_pm, inner_ops, triangles (+ n/m columns before)
