@@ -203,11 +203,20 @@ TL_API const char* tl_phase_name(int i);
  *                       probe, timing only); ignored otherwise;
  *   TL_DEBUG_CLASS_WORK 1: each tl_list also reports the inner_ops of every
  *                       seed class through tl_phase_times ("work_*", counts);
- *   TL_DEBUG_H_WIDE_MIN_N  class-H seeds run on the CTA-per-seed kernel with a
- *                       2^19 window when n exceeds this (default 2^25), so tests
- *                       on small graphs can force that path with 0.
+ *   TL_DEBUG_H_WIDE_MIN_N  when n exceeds this (default 2^25) class-H seeds run
+ *                       on the CTA-per-seed kernel with a 2^19 window and class
+ *                       C1 uses its 2^19-window instance, so tests on small
+ *                       graphs can force those paths with 0.
+ *   TL_DEBUG_H_SPLIT    above that n, class-H seeds of |S| <= value stay on the
+ *                       warp-per-seed kernel (0: all of class H goes CTA-wide).
  * Settings persist for the context. */
-enum { TL_DEBUG_BM_SHRINK = 1, TL_DEBUG_VARIANT = 2, TL_DEBUG_CLASS_WORK = 3, TL_DEBUG_H_WIDE_MIN_N = 4 };
+enum {
+    TL_DEBUG_BM_SHRINK = 1,
+    TL_DEBUG_VARIANT = 2,
+    TL_DEBUG_CLASS_WORK = 3,
+    TL_DEBUG_H_WIDE_MIN_N = 4,
+    TL_DEBUG_H_SPLIT = 5
+};
 TL_API tl_status tl_debug_set(tl_ctx* ctx, int key, int value);
 
 #ifdef __cplusplus

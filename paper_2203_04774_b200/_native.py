@@ -40,6 +40,7 @@ TL_DEBUG_BM_SHRINK = 1
 TL_DEBUG_VARIANT = 2
 TL_DEBUG_CLASS_WORK = 3
 TL_DEBUG_H_WIDE_MIN_N = 4
+TL_DEBUG_H_SPLIT = 5
 
 # every exported symbol of include/trigpu.h (tests check the .so exports all)
 TRIGPU_SYMBOLS = (

@@ -1024,7 +1024,7 @@ struct CtaCfg {
 #define TRIGPU_C1_RING 0
 #endif
 #ifndef TRIGPU_C1_MINB
-#define TRIGPU_C1_MINB 3
+#define TRIGPU_C1_MINB 2
 #endif
 #ifndef TRIGPU_C2_RING
 #define TRIGPU_C2_RING 0
@@ -1045,18 +1045,23 @@ struct CtaCfg {
 #define TRIGPU_H_BITS_A_CTA 17
 #endif
 #ifndef TRIGPU_HW_BITS_A
-#define TRIGPU_HW_BITS_A 18
+#define TRIGPU_HW_BITS_A 19
 #endif
 #ifndef TRIGPU_HW_MINB
-#define TRIGPU_HW_MINB 4
+#define TRIGPU_HW_MINB 2
 #endif
 #ifndef TRIGPU_C1_THREADS
-#define TRIGPU_C1_THREADS 256
+#define TRIGPU_C1_THREADS 512
 #endif
 #ifndef TRIGPU_HW_THREADS
-#define TRIGPU_HW_THREADS 256
+#define TRIGPU_HW_THREADS 512
 #endif
-using CfgC1 = CtaCfg<TRIGPU_C1_THREADS, TRIGPU_C1_BITS_A, 14, 1024, TRIGPU_C1_MINB, TRIGPU_C1_RING>;  // (2^17 window at 4 CTAs/SM: C4 -1 %, C5 +4 %)
+// C1: 16-warp CTAs, 2 per SM at 64 registers. Measured (C5 / C4 class time, ms):
+// 8 warps x 3 CTAs, 2^18 window 927 / 73.1; x 4 CTAs 1021 / 78.5; 16 warps x 2,
+// 2^18 902 / 69.1; 16 warps x 2, 2^19 783 / 71.9; 32 warps x 1, 2^19 807 / 72.3.
+// The 2^19 window is used above kWideMinN vertices (as for class H).
+using CfgC1 = CtaCfg<TRIGPU_C1_THREADS, TRIGPU_C1_BITS_A, 14, 1024, TRIGPU_C1_MINB, TRIGPU_C1_RING>;
+using CfgC1Wide = CtaCfg<TRIGPU_C1_THREADS, TRIGPU_C1_BITS_A + 1, 14, 1024, TRIGPU_C1_MINB, TRIGPU_C1_RING>;
 #ifndef TRIGPU_C2_BITS_A
 #define TRIGPU_C2_BITS_A 19
 #endif
@@ -1068,11 +1073,15 @@ using CfgH = CtaCfg<256, TRIGPU_H_BITS_A_CTA, 13, 256, TRIGPU_H_MINB, TRIGPU_H_R
 // Class H on graphs of more than 2^25 vertices: the set of an H seed spans so
 // many ranks that the per-warp 2^16 window leaves many of its elements to the
 // filter + verification path; a CTA per seed shares one wider window
-// (measured on C5: warp kernel 1275 ms, CTA-wide 2^19 window at 3 CTAs/SM
-// 1147 ms, 2^18 window at 4 CTAs/SM and 64 registers 1097 ms; on C4 the warp
-// kernel stays faster).
+// (measured on C5: warp kernel 1275 ms; CTA-wide, 8 warps x 3 CTAs/SM, 2^19
+// window 1147 ms; 8 warps x 4, 2^18 1097 ms; 16 warps x 2, 2^19 1082 ms; 32
+// warps x 1 1288 ms; on C4 the warp kernel stays faster).
 using CfgHWide = CtaCfg<TRIGPU_HW_THREADS, TRIGPU_HW_BITS_A, 13, 256, TRIGPU_HW_MINB, 0>;
 constexpr uint32_t kHWideMinN = 1u << 25;
+#ifndef TRIGPU_H_SPLIT
+#define TRIGPU_H_SPLIT 0
+#endif
+constexpr uint32_t kHSplit = TRIGPU_H_SPLIT;  // above kHWideMinN vertices, class-H seeds of |S| <= kHSplit stay on the warp kernel
 template <class CFG>
 constexpr size_t cta_bitmap_bytes() { return win_bytes(CFG::kBitsA, CFG::kBitsB); }
 template <class CFG>
@@ -1354,7 +1363,9 @@ constexpr int kClasses = 5;  // R, H, C1, C2, G
 
 struct SeedLists {
     uint32_t* lists[kClasses];
-    unsigned int* counts;     // [kClasses]
+    unsigned int* counts;     // [kClasses], then [kClasses] = the small class-H seeds
+    uint32_t cap;             // entries per list
+    uint32_t h_small;         // class-H seeds of |S| <= h_small go to the BACK of lists[1] (0: no split)
 };
 
 // Seeds with rank in [rb, re) and |S| >= 2 into their class lists.
@@ -1370,15 +1381,20 @@ __global__ void __launch_bounds__(256) k_classify_seeds(uint32_t rb, uint32_t re
         if (r < re) d = set_len[r];
         int cls = -1;
         if (d >= 2) cls = d <= 32 ? 0 : d <= 256 ? 1 : d <= CfgC1::kMaxD ? 2 : d <= CfgC2::kMaxD ? 3 : 4;
+        if (cls == 1 && d <= L.h_small) cls = kClasses;  // the two H lists share lists[1]: front and back
 #pragma unroll
-        for (int c = 0; c < kClasses; ++c) {
+        for (int c = 0; c <= kClasses; ++c) {
             const unsigned b = __ballot_sync(FULL, cls == c);
             if (!b) continue;
             const unsigned leader = __ffs(b) - 1;
             unsigned base = 0;
             if (lane_id() == leader) base = atomicAdd(&L.counts[c], __popc(b));
             base = __shfl_sync(FULL, base, leader);
-            if (cls == c) L.lists[c][base + __popc(b & lanemask_lt())] = (uint32_t)r;
+            const unsigned pos = base + __popc(b & lanemask_lt());
+            if (cls == c) {
+                if (c < kClasses) L.lists[c][pos] = (uint32_t)r;
+                else L.lists[1][L.cap - 1u - pos] = (uint32_t)r;
+            }
         }
     }
 }

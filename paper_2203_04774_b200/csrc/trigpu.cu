@@ -120,7 +120,8 @@ struct tl_ctx {
     int variant = 0;         // TL_DEBUG_VARIANT: probe flavour of an experiments build (A/B timing)
     uint32_t bm_shrink = 0;  // TL_DEBUG_BM_SHRINK: smaller bitmaps (tests force the filter path)
     bool class_work = false; // TL_DEBUG_CLASS_WORK: per-class inner_ops into the phase table
-    uint32_t h_wide_min_n = kHWideMinN;  // TL_DEBUG_H_WIDE_MIN_N: class H runs CTA-wide above this n
+    uint32_t h_split = kHSplit;  // TL_DEBUG_H_SPLIT: above h_wide_min_n, class-H seeds up to this |S| stay on the warp kernel
+    uint32_t h_wide_min_n = kHWideMinN;  // TL_DEBUG_H_WIDE_MIN_N: above this n class H runs CTA-wide and C1 uses the 2^19 window
     unsigned long long tri_count = 0;
 
     tl_status fail(tl_status st, const std::string& what) {
@@ -490,8 +491,8 @@ tl_status launch_cta(tl_ctx* ctx, ListParams p, uint32_t* list, unsigned count, 
 }
 
 template <int ALGO, unsigned F>
-tl_status launch_classes(tl_ctx* ctx, ListParams base, uint32_t* const lists[kClasses], const unsigned h[kClasses],
-                         unsigned int* queues) {
+tl_status launch_classes(tl_ctx* ctx, ListParams base, uint32_t* const lists[kClasses],
+                         const unsigned h[kClasses + 1], unsigned int* queues) {
     tl_status st;
     // class G first, on the side stream: a few long CTAs overlap the rest
     if (h[4]) {
@@ -537,7 +538,23 @@ tl_status launch_classes(tl_ctx* ctx, ListParams base, uint32_t* const lists[kCl
         CK(cudaEventRecord(ctx->cls_ev[1], ctx->s));
         ctx->cls_run[0] = true;
     }
+    if (h[kClasses]) {  // small class-H seeds of a large graph: warp per seed (back of lists[1])
+        ListParams p = base;
+        p.seeds = lists[1] + (ctx->n - h[kClasses]);
+        p.nseeds = h[kClasses];
+        p.queue = queues + 5;
+        const size_t smem = smem_warp<F>();
+        if ((st = set_smem(ctx, k_list_warp<ALGO, F>, smem)) != TL_OK) return st;
+        const unsigned grid = std::min<unsigned>(grid_for((uint64_t)h[kClasses] * 32, kHWarps * 32, ~0u),
+                                                 resident_grid(ctx, k_list_warp<ALGO, F>, kHWarps * 32, smem));
+        CK(cudaEventRecord(ctx->cls_ev[2], ctx->s));
+        k_list_warp<ALGO, F><<<grid, kHWarps * 32, smem, ctx->s>>>(p);
+        LAUNCHED();
+        CK(cudaEventRecord(ctx->cls_ev[3], ctx->s));
+        ctx->cls_run[1] = true;
+    }
     if (h[1]) {
+        const bool first = !h[kClasses];  // the H time spans both launches
 #if TRIGPU_H_CTA
         CK(cudaEventRecord(ctx->cls_ev[2], ctx->s));
         st = launch_cta<ALGO, F, CfgH>(ctx, base, lists[1], h[1], queues + 1);
@@ -545,7 +562,7 @@ tl_status launch_classes(tl_ctx* ctx, ListParams base, uint32_t* const lists[kCl
         CK(cudaEventRecord(ctx->cls_ev[3], ctx->s));
 #else
       if (ctx->n > ctx->h_wide_min_n) {
-        CK(cudaEventRecord(ctx->cls_ev[2], ctx->s));
+        if (first) CK(cudaEventRecord(ctx->cls_ev[2], ctx->s));
         st = launch_cta<ALGO, F, CfgHWide>(ctx, base, lists[1], h[1], queues + 1);
         if (st != TL_OK) return st;
         CK(cudaEventRecord(ctx->cls_ev[3], ctx->s));
@@ -568,7 +585,8 @@ tl_status launch_classes(tl_ctx* ctx, ListParams base, uint32_t* const lists[kCl
     }
     if (h[2]) {
         CK(cudaEventRecord(ctx->cls_ev[4], ctx->s));
-        st = launch_cta<ALGO, F, CfgC1>(ctx, base, lists[2], h[2], queues + 2);
+        st = ctx->n > ctx->h_wide_min_n ? launch_cta<ALGO, F, CfgC1Wide>(ctx, base, lists[2], h[2], queues + 2)
+                                        : launch_cta<ALGO, F, CfgC1>(ctx, base, lists[2], h[2], queues + 2);
         if (st != TL_OK) return st;
         CK(cudaEventRecord(ctx->cls_ev[5], ctx->s));
         ctx->cls_run[2] = true;
@@ -585,8 +603,8 @@ tl_status launch_classes(tl_ctx* ctx, ListParams base, uint32_t* const lists[kCl
 }
 
 template <int ALGO>
-tl_status launch_flags(tl_ctx* ctx, unsigned F, ListParams base, uint32_t* const lists[kClasses], const unsigned h[kClasses],
-                       unsigned int* queues) {
+tl_status launch_flags(tl_ctx* ctx, unsigned F, ListParams base, uint32_t* const lists[kClasses],
+                       const unsigned h[kClasses + 1], unsigned int* queues) {
     switch (F & 7u) {
         case 0: return launch_classes<ALGO, 0>(ctx, base, lists, h, queues);
         case 1: return launch_classes<ALGO, 1>(ctx, base, lists, h, queues);
@@ -1143,7 +1161,10 @@ TL_API tl_status tl_list_range(tl_ctx* ctx, int algo, unsigned out_flags, uint32
     CK(cudaMemsetAsync(counts, 0, 16 * sizeof(unsigned int), ctx->s));
     uint32_t* L = P<uint32_t>(ctx->lists);
     uint32_t* const lists[kClasses] = {L, L + n, L + 2 * (uint64_t)n, L + 3 * (uint64_t)n, L + 4 * (uint64_t)n};
-    SeedLists SL{{lists[0], lists[1], lists[2], lists[3], lists[4]}, counts};
+    // class H in two lists (front / back of lists[1]) when the graph is large: seeds of
+    // |S| <= h_split stay on the warp kernel, the others go CTA-wide
+    const uint32_t h_small = n > ctx->h_wide_min_n ? ctx->h_split : 0u;
+    SeedLists SL{{lists[0], lists[1], lists[2], lists[3], lists[4]}, counts, n, h_small};
     if (rank_end > rank_begin) {
         k_classify_seeds<<<grid_for(rank_end - rank_begin, 256, ctx->sms * 16), 256, 0, ctx->s>>>(
             rank_begin, rank_end, base.set_len, SL);
@@ -1161,7 +1182,7 @@ TL_API tl_status tl_list_range(tl_ctx* ctx, int algo, unsigned out_flags, uint32
         CK(cudaMemcpyAsync(range_ops, rc, 16, cudaMemcpyDeviceToHost, ctx->s));
     }
     CK(cudaEventRecord(ctx->ev[PH_CLASSIFY], ctx->s));
-    unsigned h[kClasses];
+    unsigned h[kClasses + 1];  // [kClasses] = small class-H seeds
     CK(cudaMemcpyAsync(h, counts, sizeof(h), cudaMemcpyDeviceToHost, ctx->s));
     CK(cudaStreamSynchronize(ctx->s));
     if (ctx->class_work) {  // per-class inner_ops (debug; outside the timed listing)
@@ -1173,6 +1194,12 @@ TL_API tl_status tl_list_range(tl_ctx* ctx, int algo, unsigned out_flags, uint32
                     lists[c], h[c], base.set_off, base.set_len, base.set_adj, base.out_len, wk + c);
                 LAUNCHED();
             }
+        if (h[kClasses]) {
+            k_class_work<<<grid_for((uint64_t)h[kClasses] * 32, 256, ctx->sms * 16), 256, 0, ctx->s>>>(
+                lists[1] + (n - h[kClasses]), h[kClasses], base.set_off, base.set_len, base.set_adj, base.out_len,
+                wk + 1);
+            LAUNCHED();
+        }
         unsigned long long w[kClasses];
         CK(cudaMemcpyAsync(w, wk, sizeof(w), cudaMemcpyDeviceToHost, ctx->s));
         CK(cudaStreamSynchronize(ctx->s));
@@ -1508,6 +1535,11 @@ TL_API tl_status tl_debug_set(tl_ctx* ctx, int key, int value) {
     }
     if (key == TL_DEBUG_H_WIDE_MIN_N) {
         ctx->h_wide_min_n = static_cast<uint32_t>(value);
+        return TL_OK;
+    }
+    if (key == TL_DEBUG_H_SPLIT) {
+        if (value < 0 || value > 256) return ctx->fail(TL_ERR_INVALID_ARGUMENT, "tl_debug_set: H split must be in [0, 256]");
+        ctx->h_split = static_cast<uint32_t>(value);
         return TL_OK;
     }
     return ctx->fail(TL_ERR_INVALID_ARGUMENT, "tl_debug_set: unknown key");

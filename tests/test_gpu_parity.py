@@ -12,8 +12,9 @@ import pytest
 import oracle
 import paper_2203_04774_b200 as tg
 from paper_2203_04774_b200 import host
-from paper_2203_04774_b200._native import (TL_ALGO_APM, TL_ALGO_APP, TL_DEBUG_BM_SHRINK, TL_DEBUG_H_WIDE_MIN_N,
-                                           TL_OUT_CHECKSUM, TL_OUT_LIST, TL_OUT_VERTEX_COUNTS)
+from paper_2203_04774_b200._native import (TL_ALGO_APM, TL_ALGO_APP, TL_DEBUG_BM_SHRINK, TL_DEBUG_H_SPLIT,
+                                           TL_DEBUG_H_WIDE_MIN_N, TL_OUT_CHECKSUM, TL_OUT_LIST,
+                                           TL_OUT_VERTEX_COUNTS)
 from golden_io import case_csr, cases, golden, sha, sweep_graphs
 
 pytestmark = pytest.mark.gpu
@@ -293,18 +294,23 @@ def test_probe_filter_path(shrink):
 
 
 def test_wide_h_path():
-    """Class H on the CTA-per-seed 2^19-window kernel (the path graphs above
-    2^25 vertices take), forced on graphs the oracle checks in seconds, with
-    and without shrunken windows (filter + verification path)."""
+    """Class H on the CTA-per-seed 2^19-window kernel and C1 on its 2^19-window
+    instance (the paths graphs above 2^25 vertices take), forced on graphs the
+    oracle checks in seconds, with and without shrunken windows (filter +
+    verification path), and with class H split between the warp kernel (small
+    sets, back of the list) and the CTA kernel (TL_DEBUG_H_SPLIT)."""
     c = tg.Context(0)
     c.debug_set(TL_DEBUG_H_WIDE_MIN_N, 0)
     try:
-        for shrink in (0, 6):
+        for shrink, split in ((0, 0), (6, 0), (0, 64), (6, 100), (0, 256)):
             c.debug_set(TL_DEBUG_BM_SHRINK, shrink)
+            c.debug_set(TL_DEBUG_H_SPLIT, split)
             for g in (tg.gen_rmat(16, 16, 5), tg.gen_chung_lu(100000, 1600000, seed=6)):
                 for meth in ("degree", "split"):
                     pi, _ = host.compute_order(g, meth)
                     _oracle_check(c, g, pi, lists=(shrink == 0))
+        with pytest.raises(ValueError):
+            c.debug_set(TL_DEBUG_H_SPLIT, 257)
     finally:
         c.close()
 

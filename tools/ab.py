@@ -19,7 +19,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
 import paper_2203_04774_b200 as tg  # noqa: E402
 from paper_2203_04774_b200 import _native  # noqa: E402
-from paper_2203_04774_b200._native import TL_DEBUG_CLASS_WORK, TL_DEBUG_VARIANT  # noqa: E402
+from paper_2203_04774_b200._native import (TL_DEBUG_CLASS_WORK, TL_DEBUG_H_SPLIT, TL_DEBUG_H_WIDE_MIN_N,
+                                           TL_DEBUG_VARIANT)  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c4")
@@ -30,6 +31,8 @@ ap.add_argument("--libs", default="base")
 ap.add_argument("--variant", type=int, default=0)
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--class-work", action="store_true", help="report per-class inner_ops and GB/s")
+ap.add_argument("--hsplit", default="", help="comma list of TL_DEBUG_H_SPLIT values to time (per library)")
+ap.add_argument("--hwide-min-n", type=int, default=-1, help="TL_DEBUG_H_WIDE_MIN_N (0: class H always CTA-wide)")
 a = ap.parse_args()
 t0 = time.perf_counter()
 g = bench.make_graph(bench.CONFIGS[a.config])
@@ -48,7 +51,12 @@ for lib in a.libs.split(","):
         ctx.debug_set(TL_DEBUG_VARIANT, a.variant)
     if a.class_work:
         ctx.debug_set(TL_DEBUG_CLASS_WORK, 1)
-    for flags in (int(f) for f in a.flags.split(",")):
+    if a.hwide_min_n >= 0:
+        ctx.debug_set(TL_DEBUG_H_WIDE_MIN_N, a.hwide_min_n)
+    splits = [int(x) for x in a.hsplit.split(",")] if a.hsplit else [None]
+    for flags, hsplit in ((int(f), sp) for f in a.flags.split(",") for sp in splits):
+        if hsplit is not None:
+            ctx.debug_set(TL_DEBUG_H_SPLIT, hsplit)
         st = ctx.list(algo, flags)
         if ref is None:
             ref = st.triangle_count
@@ -68,7 +76,7 @@ for lib in a.libs.split(","):
                     mean["gbs_" + c] = round(4 * w / (mean["list_" + c] / 1e3) / 1e9, 1)
         B = 4 * (st.inner_ops + 2 * g.m)
         print(json.dumps({"config": a.config, "ordering": a.ordering, "algo": a.algo, "flags": flags,
-                          "variant": a.variant, "lib": lib, "T": st.triangle_count, "checksum": st.checksum,
+                          "variant": a.variant, "lib": lib, "hwide_min_n": a.hwide_min_n, "hsplit": hsplit, "T": st.triangle_count, "checksum": st.checksum,
                           "C": st.inner_ops, "m": g.m, "frac": round(B / (mean["list"] / 1e3) / 6550.1e9, 4),
                           "orient_ms": round(st.orient_ms, 2), "gen_s": round(gen_s, 1), **mean}), flush=True)
     ctx.close()
