@@ -203,12 +203,14 @@ TL_API const char* tl_phase_name(int i);
  *                       probe, timing only); ignored otherwise;
  *   TL_DEBUG_CLASS_WORK 1: each tl_list also reports the inner_ops of every
  *                       seed class through tl_phase_times ("work_*", counts);
- *   TL_DEBUG_H_WIDE_MIN_N  when n exceeds this (default 2^25) class-H seeds run
- *                       on the CTA-per-seed kernel with a 2^19 window and class
- *                       C1 uses its 2^19-window instance, so tests on small
- *                       graphs can force those paths with 0.
- *   TL_DEBUG_H_SPLIT    above that n, class-H seeds of |S| <= value stay on the
- *                       warp-per-seed kernel (0: all of class H goes CTA-wide).
+ *   TL_DEBUG_H_WIDE_MIN_N  the graph-size thresholds above which class H is
+ *                       split between the warp and the CTA kernel (default
+ *                       2^23 vertices) and class C1 uses its 2^19-window
+ *                       instance (default 2^25): both are set to this value,
+ *                       so tests on small graphs force those paths with 0;
+ *   TL_DEBUG_H_SPLIT    largest class-H |S| left on the warp-per-seed kernel
+ *                       when class H is split (default 96; 0: all CTA, 256:
+ *                       all warp).
  * Settings persist for the context. */
 enum {
     TL_DEBUG_BM_SHRINK = 1,

@@ -12,10 +12,14 @@
 // The reference's uint8 table[n] (listing.hpp:113) becomes a per-seed
 // windowed bitmap in shared memory sized to the class of |S| (degree binning):
 //   class R  2 <= |S| <= 32     warp per seed, 2^15-bit window per warp
-//   class H  32 < |S| <= 256    warp per seed, 2^16-bit window per warp
-//   class C1 256 < |S| <= 1024  CTA (8 warps) per seed, 2^18-bit window
+//   class H  32 < |S| <= 256    warp per seed, 2^16-bit window per warp; on graphs
+//                               of more than 2^23 vertices only up to |S| = 96, the
+//                               larger sets on a CTA (16 warps) per seed, 2^19 window
+//   class C1 256 < |S| <= 1024  CTA (16 warps) per seed, 2^18-bit window (2^19 above
+//                               2^25 vertices)
 //   class C2 1024 < |S| <= 4096 CTA (32 warps) per seed, 2^19-bit window
-//   class G  |S| > 4096         CTA per seed, n-bit bitmap in global memory
+//   class G  |S| > 4096         CTA per seed, 2^20-bit window + coarse filter in
+//                               shared memory over an exact n-bit bitmap in global memory
 // Every class reads the out-rows of the seed's set as 128-element chunks of
 // 16-byte quads (one 512-byte warp load per chunk, four chunks in flight);
 // rows shorter than kLongRow are walked as one flattened stream over 32 rows.
@@ -1077,11 +1081,21 @@ using CfgH = CtaCfg<256, TRIGPU_H_BITS_A_CTA, 13, 256, TRIGPU_H_MINB, TRIGPU_H_R
 // window 1147 ms; 8 warps x 4, 2^18 1097 ms; 16 warps x 2, 2^19 1082 ms; 32
 // warps x 1 1288 ms; on C4 the warp kernel stays faster).
 using CfgHWide = CtaCfg<TRIGPU_HW_THREADS, TRIGPU_HW_BITS_A, 13, 256, TRIGPU_HW_MINB, 0>;
-constexpr uint32_t kHWideMinN = 1u << 25;
-#ifndef TRIGPU_H_SPLIT
-#define TRIGPU_H_SPLIT 0
+// Graph-size thresholds: above kHCtaMinN vertices class H is split - seeds of
+// |S| <= kHSplit stay on the warp-per-seed kernel (cheap set-up, windows that
+// still cover a small set), the larger sets go to the CTA kernel; above
+// kWideMinN vertices C1 uses its 2^19-window instance. (C5 class H: all CTA
+// 1087 ms, split at 64 / 96 / 128: 1074 / 1051 / 1050, all warp 1279; C4: all
+// warp 74.2, split at 64: 70.5, all CTA 74.1.)
+constexpr uint32_t kWideMinN = 1u << 25;
+#ifndef TRIGPU_H_CTA_MIN_N
+#define TRIGPU_H_CTA_MIN_N (1u << 23)
 #endif
-constexpr uint32_t kHSplit = TRIGPU_H_SPLIT;  // above kHWideMinN vertices, class-H seeds of |S| <= kHSplit stay on the warp kernel
+constexpr uint32_t kHCtaMinN = TRIGPU_H_CTA_MIN_N;
+#ifndef TRIGPU_H_SPLIT
+#define TRIGPU_H_SPLIT 96
+#endif
+constexpr uint32_t kHSplit = TRIGPU_H_SPLIT;
 template <class CFG>
 constexpr size_t cta_bitmap_bytes() { return win_bytes(CFG::kBitsA, CFG::kBitsB); }
 template <class CFG>

@@ -120,8 +120,9 @@ struct tl_ctx {
     int variant = 0;         // TL_DEBUG_VARIANT: probe flavour of an experiments build (A/B timing)
     uint32_t bm_shrink = 0;  // TL_DEBUG_BM_SHRINK: smaller bitmaps (tests force the filter path)
     bool class_work = false; // TL_DEBUG_CLASS_WORK: per-class inner_ops into the phase table
-    uint32_t h_split = kHSplit;  // TL_DEBUG_H_SPLIT: above h_wide_min_n, class-H seeds up to this |S| stay on the warp kernel
-    uint32_t h_wide_min_n = kHWideMinN;  // TL_DEBUG_H_WIDE_MIN_N: above this n class H runs CTA-wide and C1 uses the 2^19 window
+    uint32_t h_split = kHSplit;        // TL_DEBUG_H_SPLIT: largest class-H |S| left on the warp kernel above h_cta_min_n
+    uint32_t h_cta_min_n = kHCtaMinN;  // TL_DEBUG_H_WIDE_MIN_N sets both thresholds (tests force the paths with 0):
+    uint32_t wide_min_n = kWideMinN;   //   class H split above h_cta_min_n, C1's 2^19 window above wide_min_n
     unsigned long long tri_count = 0;
 
     tl_status fail(tl_status st, const std::string& what) {
@@ -561,7 +562,7 @@ tl_status launch_classes(tl_ctx* ctx, ListParams base, uint32_t* const lists[kCl
         if (st != TL_OK) return st;
         CK(cudaEventRecord(ctx->cls_ev[3], ctx->s));
 #else
-      if (ctx->n > ctx->h_wide_min_n) {
+      if (ctx->n > ctx->h_cta_min_n) {
         if (first) CK(cudaEventRecord(ctx->cls_ev[2], ctx->s));
         st = launch_cta<ALGO, F, CfgHWide>(ctx, base, lists[1], h[1], queues + 1);
         if (st != TL_OK) return st;
@@ -585,7 +586,7 @@ tl_status launch_classes(tl_ctx* ctx, ListParams base, uint32_t* const lists[kCl
     }
     if (h[2]) {
         CK(cudaEventRecord(ctx->cls_ev[4], ctx->s));
-        st = ctx->n > ctx->h_wide_min_n ? launch_cta<ALGO, F, CfgC1Wide>(ctx, base, lists[2], h[2], queues + 2)
+        st = ctx->n > ctx->wide_min_n ? launch_cta<ALGO, F, CfgC1Wide>(ctx, base, lists[2], h[2], queues + 2)
                                         : launch_cta<ALGO, F, CfgC1>(ctx, base, lists[2], h[2], queues + 2);
         if (st != TL_OK) return st;
         CK(cudaEventRecord(ctx->cls_ev[5], ctx->s));
@@ -1163,7 +1164,7 @@ TL_API tl_status tl_list_range(tl_ctx* ctx, int algo, unsigned out_flags, uint32
     uint32_t* const lists[kClasses] = {L, L + n, L + 2 * (uint64_t)n, L + 3 * (uint64_t)n, L + 4 * (uint64_t)n};
     // class H in two lists (front / back of lists[1]) when the graph is large: seeds of
     // |S| <= h_split stay on the warp kernel, the others go CTA-wide
-    const uint32_t h_small = n > ctx->h_wide_min_n ? ctx->h_split : 0u;
+    const uint32_t h_small = n > ctx->h_cta_min_n ? ctx->h_split : 0u;
     SeedLists SL{{lists[0], lists[1], lists[2], lists[3], lists[4]}, counts, n, h_small};
     if (rank_end > rank_begin) {
         k_classify_seeds<<<grid_for(rank_end - rank_begin, 256, ctx->sms * 16), 256, 0, ctx->s>>>(
@@ -1534,7 +1535,7 @@ TL_API tl_status tl_debug_set(tl_ctx* ctx, int key, int value) {
         return TL_OK;
     }
     if (key == TL_DEBUG_H_WIDE_MIN_N) {
-        ctx->h_wide_min_n = static_cast<uint32_t>(value);
+        ctx->h_cta_min_n = ctx->wide_min_n = static_cast<uint32_t>(value);
         return TL_OK;
     }
     if (key == TL_DEBUG_H_SPLIT) {
