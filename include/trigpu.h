@@ -205,7 +205,7 @@ TL_API const char* tl_phase_name(int i);
  *                       seed class through tl_phase_times ("work_*", counts);
  *   TL_DEBUG_H_WIDE_MIN_N  the graph-size thresholds above which class H is
  *                       split between the warp and the CTA kernel (default
- *                       2^23 vertices) and class C1 uses its 2^19-window
+ *                       2^21 vertices) and class C1 uses its 2^19-window
  *                       instance (default 2^25): both are set to this value,
  *                       so tests on small graphs force those paths with 0;
  *   TL_DEBUG_H_SPLIT    largest class-H |S| left on the warp-per-seed kernel

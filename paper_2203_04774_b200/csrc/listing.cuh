@@ -13,7 +13,7 @@
 // windowed bitmap in shared memory sized to the class of |S| (degree binning):
 //   class R  2 <= |S| <= 32     warp per seed, 2^15-bit window per warp
 //   class H  32 < |S| <= 256    warp per seed, 2^16-bit window per warp; on graphs
-//                               of more than 2^23 vertices only up to |S| = 96, the
+//                               of more than 2^21 vertices only up to |S| = 96, the
 //                               larger sets on a CTA (16 warps) per seed, 2^19 window
 //   class C1 256 < |S| <= 1024  CTA (16 warps) per seed, 2^18-bit window (2^19 above
 //                               2^25 vertices)
@@ -655,20 +655,66 @@ struct CtaRowCursor {
     }
 };
 
+// Chunks [c, ce) of ONE row (a CTA's warps sharing a giant row).
+struct RowRangeCursor {
+    uint32_t q0, nqr, x, c, ce;
+    __device__ __forceinline__ bool more() const { return c < ce; }
+    template <int N>
+    __device__ __forceinline__ void next(Chunk (&ch)[N]) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            if (c < ce) {
+                ch[i] = Chunk{q0 + 32u * c, min(32u, nqr - 32u * c), x};
+                ++c;
+            } else {
+                ch[i] = Chunk{0, 0, 0};
+            }
+        }
+    }
+};
+
+// Rows a warp does not stream itself: the class G kernel collects the giant
+// rows of a seed (>= kDeferQuads quads) in a shared list and its 32 warps
+// stream each of them together afterwards - a single warp walking a
+// million-element hub row is what the rest of the CTA waits for at the seed's
+// barrier (ncu, C4 split order: barrier stall 10 per issue).
+constexpr uint32_t kDeferQuads = 4096;  // 16 K elements: 128 chunks, one batch per warp
+constexpr uint32_t kDeferCap = 1024;    // rows per seed; a full list falls back to the warp's own walk
+struct NoDefer {
+    static constexpr bool enabled = false;
+    __device__ __forceinline__ bool push(uint32_t, uint32_t, uint32_t) const { return false; }
+};
+struct SharedRowList {
+    static constexpr bool enabled = true;
+    unsigned rows;        // shared address of kDeferCap uint4 {first quad, quads, x, -}
+    unsigned int* count;  // shared counter
+    __device__ __forceinline__ bool push(uint32_t q0, uint32_t nq, uint32_t x) const {
+        const unsigned slot = atomicAdd(count, 1u);
+        if (slot >= kDeferCap) return false;
+        sts128(rows + 16u * slot, make_uint4(q0, nq, x, 0u));
+        return true;
+    }
+};
+
 // Walk the out-rows of up to 32 x's (x valid on lanes with xvalid), probing
 // every element y against the seed's set:
 //   1. rows of >= kLongRow elements as quad chunks (stream_quads);
 //   2. shorter rows as ONE flattened stream (lane f of a window reads
 //      element f of the concatenated rows; the owning row of each lane comes
 //      from an OR-reduction of the row starts), so short rows do not idle lanes.
-template <int ALGO, unsigned F, class Probe>
+template <int ALGO, unsigned F, class Probe, class Defer = NoDefer>
 __device__ __forceinline__ void scan_rows_at(const ListParams& P, uint32_t seed, uint32_t x, uint64_t ro, uint32_t rl,
-                                             const Probe& probe, Sink<ALGO, F>& sink) {
+                                             const Probe& probe, Sink<ALGO, F>& sink, const Defer& defer = Defer{}) {
     const unsigned lane = lane_id();
     unsigned hits = 0;
     // ---- phase 1: long rows, quad chunks
     {
-        LaneRowCursor cur(static_cast<uint32_t>(ro >> 2), (rl + 3u) >> 2, x, __ballot_sync(FULL, rl >= kLongRow));
+        bool mine = rl >= kLongRow;
+        if constexpr (Defer::enabled) {
+            const uint32_t nq = (rl + 3u) >> 2;
+            if (mine && nq >= kDeferQuads && defer.push(static_cast<uint32_t>(ro >> 2), nq, x)) mine = false;
+        }
+        LaneRowCursor cur(static_cast<uint32_t>(ro >> 2), (rl + 3u) >> 2, x, __ballot_sync(FULL, mine));
         stream_quads<ALGO, F, true>(P, seed, cur, probe, sink, hits);
     }
     if (rl >= kLongRow) rl = 0;
@@ -740,30 +786,31 @@ __device__ __forceinline__ void scan_rows_at(const ListParams& P, uint32_t seed,
     sink.cnt += hits;
 }
 
-template <int ALGO, unsigned F, class Probe>
+template <int ALGO, unsigned F, class Probe, class Defer = NoDefer>
 __device__ __forceinline__ void scan_rows(const ListParams& P, uint32_t seed, uint32_t x, bool xvalid,
-                                          const Probe& probe, Sink<ALGO, F>& sink) {
+                                          const Probe& probe, Sink<ALGO, F>& sink, const Defer& defer = Defer{}) {
     uint64_t ro = 0;
     uint32_t rl = 0;
     if (xvalid) {
         ro = P.out_off[x];
         rl = P.out_len[x];
     }
-    scan_rows_at<ALGO, F>(P, seed, x, ro, rl, probe, sink);
+    scan_rows_at<ALGO, F>(P, seed, x, ro, rl, probe, sink, defer);
 }
 
 // Chunks of 32 x's: set elements c, c + stride, ... below xe of the seed row at so.
 // (Loading the next chunk's x's and row offsets ahead of the current chunk's
 // streaming measured 2-3 % slower for class H on C4: the extra live registers
 // cost more than the two round trips per 32 rows.)
-template <int ALGO, unsigned F, class Probe>
+template <int ALGO, unsigned F, class Probe, class Defer = NoDefer>
 __device__ __forceinline__ void scan_x_range(const ListParams& P, uint32_t seed, uint64_t so, uint32_t cb,
-                                             uint32_t xe, uint32_t stride, const Probe& probe, Sink<ALGO, F>& sink) {
+                                             uint32_t xe, uint32_t stride, const Probe& probe, Sink<ALGO, F>& sink,
+                                             const Defer& defer = Defer{}) {
     const unsigned lane = lane_id();
     for (uint32_t c = cb; c < xe; c += stride) {
         const bool xv = c + lane < xe;
         const uint32_t x = xv ? __ldg(P.set_adj + so + c + lane) : kNone;
-        scan_rows<ALGO, F>(P, seed, x, xv, probe, sink);
+        scan_rows<ALGO, F>(P, seed, x, xv, probe, sink, defer);
     }
 }
 
@@ -1086,10 +1133,11 @@ using CfgHWide = CtaCfg<TRIGPU_HW_THREADS, TRIGPU_HW_BITS_A, 13, 256, TRIGPU_HW_
 // still cover a small set), the larger sets go to the CTA kernel; above
 // kWideMinN vertices C1 uses its 2^19-window instance. (C5 class H: all CTA
 // 1087 ms, split at 64 / 96 / 128: 1074 / 1051 / 1050, all warp 1279; C4: all
-// warp 74.2, split at 64: 70.5, all CTA 74.1.)
+// warp 74.2, split at 96: 69.1, all CTA 74.1; C2, 4 M vertices: count + checksum
+// all warp 6.7, split 7.0; with per-vertex counts 15.3 vs 13.7.)
 constexpr uint32_t kWideMinN = 1u << 25;
 #ifndef TRIGPU_H_CTA_MIN_N
-#define TRIGPU_H_CTA_MIN_N (1u << 23)
+#define TRIGPU_H_CTA_MIN_N (1u << 21)
 #endif
 constexpr uint32_t kHCtaMinN = TRIGPU_H_CTA_MIN_N;
 #ifndef TRIGPU_H_SPLIT
@@ -1320,6 +1368,9 @@ __global__ void __launch_bounds__(kGThreads) k_list_giant(ListParams P) {
     uint32_t* coarse = win + kGWinBytes / 4;
     constexpr uint32_t kWords = (kGWinBytes + kGCoarseBytes) / 4;
     for (uint32_t i = threadIdx.x; i < kWords; i += kGThreads) win[i] = 0u;
+    __shared__ unsigned int giant_rows;  // rows of this seed left to the whole CTA
+    const SharedRowList defer{smem_addr(dsm + warp_scratch_bytes<F>(kGWarps) + kGWinBytes + kGCoarseBytes), &giant_rows};
+    if (threadIdx.x == 0) giant_rows = 0u;
     Sink<ALGO, F> sink;
     attach_scratch(sink, dsm);
     for (;;) {
@@ -1349,9 +1400,23 @@ __global__ void __launch_bounds__(kGThreads) k_list_giant(ListParams P) {
         }
         __syncthreads();
         const WinGlobalProbe probe{smem_addr(win), wb, la, bm, smem_addr(coarse), cs};
-        scan_x_range<ALGO, F>(P, seed, so, warp * 32, d, kGWarps * 32, probe, sink);
+        scan_x_range<ALGO, F>(P, seed, so, warp * 32, d, kGWarps * 32, probe, sink, defer);
+        __syncthreads();
+        {  // the seed's giant rows, every warp an equal share of each row's chunks
+            const unsigned nrows = min(giant_rows, kDeferCap);
+            unsigned hits = 0;
+            for (unsigned i = 0; i < nrows; ++i) {
+                const uint4 e = lds128(defer.rows + 16u * i);
+                const uint32_t nch = row_chunks(e.y);
+                RowRangeCursor cur{e.x, e.y, e.z, static_cast<uint32_t>((static_cast<uint64_t>(nch) * warp) / kGWarps),
+                                   static_cast<uint32_t>((static_cast<uint64_t>(nch) * (warp + 1)) / kGWarps)};
+                stream_quads<ALGO, F, true>(P, seed, cur, probe, sink, hits);
+            }
+            sink.cnt += hits;
+        }
         sink.end_unit(P, seed);
         __syncthreads();
+        if (threadIdx.x == 0) giant_rows = 0u;
         for (uint32_t k = threadIdx.x; k < d; k += kGThreads) {
             const uint32_t v = __ldg(row + k);
             if (v >= wb) {
@@ -1370,7 +1435,7 @@ __global__ void __launch_bounds__(kGThreads) k_list_giant(ListParams P) {
 template <unsigned F> constexpr size_t smem_reg() { return warp_scratch_bytes<F>(kRWarps) + kRWarps * kRBmBytes; }
 template <unsigned F> constexpr size_t smem_warp() { return warp_scratch_bytes<F>(kHWarps) + kHWarps * kHBmBytes; }
 template <unsigned F, class CFG> constexpr size_t smem_cta() { return warp_scratch_bytes<F>(CFG::kWarps) + cta_bitmap_bytes<CFG>() + cta_row_bytes<CFG>() + cta_ring_bytes<CFG>(); }
-template <unsigned F> constexpr size_t smem_giant() { return warp_scratch_bytes<F>(kGWarps) + kGWinBytes + kGCoarseBytes; }
+template <unsigned F> constexpr size_t smem_giant() { return warp_scratch_bytes<F>(kGWarps) + kGWinBytes + kGCoarseBytes + kDeferCap * 16; }
 
 // ---- seed classification --------------------------------------------------
 constexpr int kClasses = 5;  // R, H, C1, C2, G

@@ -151,6 +151,24 @@ def test_giant_hubs_and_long_rows(ctx):
         _oracle_check(ctx, g, pi)
 
 
+def test_giant_rows_shared_by_the_cta(ctx):
+    """Class G seeds whose sets contain rows of more than 16 K elements: those
+    rows are left to the whole CTA (every warp a share of each row's chunks)
+    instead of one warp; under the identity order seed 0 (|S| = 6000) scans the
+    30000- and 20000-element out-rows of vertices 1 and 2, and vertex 1 is a
+    class G seed itself."""
+    rng = np.random.default_rng(9)
+    n = 40000
+    e = [(0, v) for v in range(1, 6001)] + [(1, v) for v in range(2, 30002)] + [(2, v) for v in range(3, 20003)]
+    extra = rng.integers(0, n, size=(80000, 2))
+    g = tg.Graph.from_dense_edges(n, np.concatenate([np.array(e), extra]))
+    for pi in (tg.identity_order(g), host.compute_order(g, "split")[0], tg.degree_order(g)):
+        _oracle_check(ctx, g, pi)
+    # both algorithms agree with brute-force counting on the hub triangles
+    ctx.orient(g.offsets, g.adjacency, tg.identity_order(g).ranks)
+    assert ctx.list(TL_ALGO_APM, 0).triangle_count == ctx.list(TL_ALGO_APP, 0).triangle_count
+
+
 def test_dense_clique(ctx):
     n = 300
     e = np.array([(u, v) for u in range(n) for v in range(u + 1, n)])
@@ -302,7 +320,7 @@ def test_wide_h_path():
     c = tg.Context(0)
     c.debug_set(TL_DEBUG_H_WIDE_MIN_N, 0)
     try:
-        for shrink, split in ((0, 0), (6, 0), (0, 64), (6, 100), (0, 256)):
+        for shrink, split in ((0, 0), (6, 96), (0, 256)):
             c.debug_set(TL_DEBUG_BM_SHRINK, shrink)
             c.debug_set(TL_DEBUG_H_SPLIT, split)
             for g in (tg.gen_rmat(16, 16, 5), tg.gen_chung_lu(100000, 1600000, seed=6)):
