@@ -1111,8 +1111,11 @@ struct CtaCfg {
 // 8 warps x 3 CTAs, 2^18 window 927 / 73.1; x 4 CTAs 1021 / 78.5; 16 warps x 2,
 // 2^18 902 / 69.1; 16 warps x 2, 2^19 783 / 71.9; 32 warps x 1, 2^19 807 / 72.3.
 // The 2^19 window is used above kWideMinN vertices (as for class H).
-using CfgC1 = CtaCfg<TRIGPU_C1_THREADS, TRIGPU_C1_BITS_A, 14, 1024, TRIGPU_C1_MINB, TRIGPU_C1_RING>;
-using CfgC1Wide = CtaCfg<TRIGPU_C1_THREADS, TRIGPU_C1_BITS_A + 1, 14, 1024, TRIGPU_C1_MINB, TRIGPU_C1_RING>;
+#ifndef TRIGPU_C1_MAXD
+#define TRIGPU_C1_MAXD 1024
+#endif
+using CfgC1 = CtaCfg<TRIGPU_C1_THREADS, TRIGPU_C1_BITS_A, 14, TRIGPU_C1_MAXD, TRIGPU_C1_MINB, TRIGPU_C1_RING>;
+using CfgC1Wide = CtaCfg<TRIGPU_C1_THREADS, TRIGPU_C1_BITS_A + 1, 14, TRIGPU_C1_MAXD, TRIGPU_C1_MINB, TRIGPU_C1_RING>;
 #ifndef TRIGPU_C2_BITS_A
 #define TRIGPU_C2_BITS_A 19
 #endif
