@@ -132,7 +132,7 @@ SCALED = {
 
 
 @pytest.mark.parametrize("gname", list(SCALED))
-@pytest.mark.parametrize("meth", ["degree", "core", "split", "check"])
+@pytest.mark.parametrize("meth", ["degree", "core", "split", "check", "neigh"])
 def test_scaled_configs_vs_oracle(ctx, gname, meth):
     g = SCALED[gname]()
     pi, _ = host.compute_order(g, meth)
