@@ -93,7 +93,7 @@ def test_c5_full_size(ctx):
             assert np.array_equal(ctx.fetch_vertex_counts(n), exp.vcounts)
         checked += 1
         ops += exp.inner_ops
-        if checked >= 12 and ops > 2 * 10**10:
+        if checked >= 8 and ops > 10**10:  # (suite time: the oracle lists ~1 % of C5 per range set)
             break
     # a partition of the rank space adds up to the full listing
     cuts = np.linspace(0, n, 17).astype(np.int64)
