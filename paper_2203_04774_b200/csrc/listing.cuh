@@ -180,6 +180,21 @@ struct RowVerify {  // branch-free binary search of the seed's sorted set row (L
     }
 };
 
+// Class R seeds whose set is wider than the window and whose rows are all
+// short: the 5-step shuffle search over S (one key per lane) answers every
+// probe exactly, so the seed needs no bitmap at all (no set / clear, and no
+// filter + verification round, which on a Watts-Strogatz graph - sets spread
+// over all ranks, a third of the probes hitting - ran for nearly every window).
+struct SearchProbe {
+    static constexpr bool low = false;
+    RegVerify ver;
+    __device__ __forceinline__ uint32_t bit(uint32_t y) const { return ver(y, true); }
+    __device__ __forceinline__ bool below(uint32_t) const { return false; }
+    __device__ __forceinline__ uint32_t cand(uint32_t) const { return 0u; }
+    __device__ __forceinline__ bool verify(uint32_t, bool act) const { return act; }
+    __device__ __forceinline__ uint32_t sentinel() const { return kNone; }
+};
+
 // Timing-only probe (TL_DEBUG_VARIANT 2 in a -DTRIGPU_EXPERIMENTS build):
 // touches every loaded element, never hits. Measures the row-streaming limit.
 struct NullProbe {
@@ -195,7 +210,8 @@ struct NullProbe {
 // (warp-convergent: RegVerify shuffles).
 template <class Probe>
 __device__ __forceinline__ bool probe_one(const Probe& probe, uint32_t y, bool act) {
-    bool hit = act && probe.bit(y);
+    const uint32_t b = probe.bit(y);  // evaluated by every lane (SearchProbe shuffles)
+    bool hit = act && b;
     if constexpr (Probe::low) {
         const bool c = act && probe.below(y) && probe.cand(y);
         if (__any_sync(FULL, c)) hit |= probe.verify(y, c);
@@ -915,6 +931,9 @@ __device__ __forceinline__ uint32_t r_insert(uint32_t* tab, uint32_t s) {
 #ifndef TRIGPU_R_HASH
 #define TRIGPU_R_HASH 0
 #endif
+#ifndef TRIGPU_R_SEARCH
+#define TRIGPU_R_SEARCH 1  // wide sets of short rows: shuffle search instead of the bitmap
+#endif
 constexpr int kRWarps = 8;
 #ifndef TRIGPU_R_BITS_A
 #define TRIGPU_R_BITS_A 15
@@ -986,15 +1005,23 @@ __global__ void __launch_bounds__(kRWarps * 32, R_MINB(F)) k_list_reg(ListParams
 #else
             const WinGeom g =
                 win_geom(kRBitsA, kRBitsB, P.bm_shrink, __shfl_sync(FULL, s, 0), __shfl_sync(FULL, s, d - 1));
-            if (lane < d) win_set(bma, bmb, g, s);
-            __syncwarp();
-            with_win_probe(P, smem_addr(bma), smem_addr(bmb), g, RegVerify{s}, [&](const auto& probe) {
-                scan_rows_at<ALGO, F>(P, seed, s, ro, rl, probe, sink);
-            });
-            sink.end_unit(P, seed);
-            __syncwarp();
-            if (lane < d) win_clear(bma, bmb, g, s);
-            __syncwarp();
+#if TRIGPU_R_SEARCH
+            if (g.low && !__any_sync(FULL, rl >= kLongRow)) {
+                scan_rows_at<ALGO, F>(P, seed, s, ro, rl, SearchProbe{RegVerify{s}}, sink);
+                sink.end_unit(P, seed);
+            } else
+#endif
+            {
+                if (lane < d) win_set(bma, bmb, g, s);
+                __syncwarp();
+                with_win_probe(P, smem_addr(bma), smem_addr(bmb), g, RegVerify{s}, [&](const auto& probe) {
+                    scan_rows_at<ALGO, F>(P, seed, s, ro, rl, probe, sink);
+                });
+                sink.end_unit(P, seed);
+                __syncwarp();
+                if (lane < d) win_clear(bma, bmb, g, s);
+                __syncwarp();
+            }
 #endif
             // the next seed's row offsets (its set has arrived by now)
             d = d1;

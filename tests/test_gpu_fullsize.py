@@ -16,7 +16,7 @@
   byte-identical, with its SHA-256.
 * C3-1M (Watts-Strogatz, the config's full-list instance): canonical list.
 * C3 (16 M, 256 M edges) and C4 (R-MAT-24): count, checksum, per-vertex counts
-  against the reference for degree A+- (C4 also split A+- and degree A++).
+  against the reference for degree A+- (C4 also degree A++).
 """
 import hashlib
 import os
@@ -159,7 +159,11 @@ def test_c3_1m_list_vs_reference(ctx):
 @pytest.mark.parametrize("cfg", ["c3", "c4"])
 def test_full_size_counts_vs_reference(ctx, cfg):
     g = tg.gen_ws(16_000_000, 32, 0.1, seed=1) if cfg == "c3" else tg.gen_rmat(24, 16, 1)
-    runs = [("degree", TL_ALGO_APM)] + ([("degree", TL_ALGO_APP), ("split", TL_ALGO_APM)] if cfg == "c4" else [])
+    # (split A+- at full C4 size costs a second reference view + listing, ~2 minutes of the suite's
+    # budget: tools/sweep.py runs it; here split order is checked against the degree-order results
+    # at full size in test_gpu_parity.py::test_full_size_c4_properties and against the oracle on
+    # the scaled configs)
+    runs = [("degree", TL_ALGO_APM)] + ([("degree", TL_ALGO_APP)] if cfg == "c4" else [])
     rg = oracle.RefGraph.from_csr(g.offsets, g.adjacency)
     for meth in dict.fromkeys(m for m, _ in runs):
         r = rg.order(meth, 0)
