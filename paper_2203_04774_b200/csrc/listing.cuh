@@ -63,6 +63,8 @@ struct ListParams {
     uint64_t bitmap_words;
     uint32_t hot_rank;        // rows of ranks >= hot_rank (the most re-read ones) are loaded evict_last
     uint32_t hist_base;       // per-vertex counts of ranks >= hist_base are kept per CTA in shared memory
+    int r_search;             // class R: shuffle search instead of the bitmap for sets wider than the window
+                              //   (set when the graph has no long rows at all, see k_list_reg)
     int variant;              // TL_DEBUG_VARIANT: 2 = null probe (experiments build, timing only)
     uint32_t bm_shrink;       // TL_DEBUG_BM_SHRINK: smaller windows (tests force the below-window path)
 };
@@ -180,11 +182,15 @@ struct RowVerify {  // branch-free binary search of the seed's sorted set row (L
     }
 };
 
-// Class R seeds whose set is wider than the window and whose rows are all
-// short: the 5-step shuffle search over S (one key per lane) answers every
-// probe exactly, so the seed needs no bitmap at all (no set / clear, and no
-// filter + verification round, which on a Watts-Strogatz graph - sets spread
-// over all ranks, a third of the probes hitting - ran for nearly every window).
+// Class R seeds whose set is wider than the window, on graphs without long rows
+// (max d+ < kLongRow: lattice-like graphs): the 5-step shuffle search over S
+// (one key per lane) answers every probe exactly, so the seed needs no bitmap
+// at all - no set / clear and no filter + verification round, which on a
+// Watts-Strogatz graph (sets spread over all ranks, a third of the probes
+// hitting) ran for nearly every window: C3 count 12.8 -> 10.0 ms. On
+// power-law graphs hits are rare, the filter almost never fires and the
+// bitmap stays cheaper (C5 class R 320 vs 339 ms with the search), so the
+// switch is per graph.
 struct SearchProbe {
     static constexpr bool low = false;
     RegVerify ver;
@@ -1006,7 +1012,7 @@ __global__ void __launch_bounds__(kRWarps * 32, R_MINB(F)) k_list_reg(ListParams
             const WinGeom g =
                 win_geom(kRBitsA, kRBitsB, P.bm_shrink, __shfl_sync(FULL, s, 0), __shfl_sync(FULL, s, d - 1));
 #if TRIGPU_R_SEARCH
-            if (g.low && !__any_sync(FULL, rl >= kLongRow)) {
+            if (P.r_search && g.low) {
                 scan_rows_at<ALGO, F>(P, seed, s, ro, rl, SearchProbe{RegVerify{s}}, sink);
                 sink.end_unit(P, seed);
             } else

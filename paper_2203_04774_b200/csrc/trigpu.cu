@@ -1155,6 +1155,7 @@ TL_API tl_status tl_list_range(tl_ctx* ctx, int algo, unsigned out_flags, uint32
     base.vcount = want_vc ? P<unsigned long long>(ctx->vcount) : nullptr;
     base.variant = ctx->variant;
     base.hot_rank = ctx->hot_rank;
+    base.r_search = ctx->max_out < kLongRow;  // no long rows anywhere: class R searches instead of probing a bitmap
     base.hist_base = n > kHist ? n - kHist : 0;
     base.bm_shrink = ctx->bm_shrink;
 
