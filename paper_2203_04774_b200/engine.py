@@ -232,7 +232,7 @@ class Context:
         return ms.value
 
     def debug_set(self, key: int, value: int) -> None:
-        """Test-only knobs (tl_debug_set): TL_DEBUG_BM_SHRINK, TL_DEBUG_VARIANT."""
+        """Test-only knobs (tl_debug_set, include/trigpu.h): TL_DEBUG_BM_SHRINK, _VARIANT, _CLASS_WORK, _H_WIDE_MIN_N, _H_SPLIT."""
         _check(self._p, _native.trigpu().tl_debug_set(self._p, key, value))
 
     def phase_times(self) -> dict:
